@@ -1,0 +1,441 @@
+// oracle/ref_driver.cpp — TEST INFRASTRUCTURE ONLY (never linked into the product).
+//
+// Exposes the *unmodified* reference implementation (/root/reference/proj) to
+// the Python test-suite and to bench.py's CPU-baseline leg through a small
+// extern "C" surface. The reference sources are compiled in place by
+// oracle/Makefile (nothing is copied into this repository); model.cpp and
+// harness.cpp are included into this translation unit so the anonymous-
+// namespace `nmp_layer_backward` (model.cpp:318-387) is callable directly.
+//
+// Output: oracle/_ref/libhgnn_ref.so (git-ignored, travels to the GPU box).
+
+#include "model.cpp"    // NOLINT: reference TU, compiled in place (src/model.cpp)
+#include "harness.cpp"  // NOLINT: reference TU (src/harness.cpp) for tgv/verify_partition
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+// io.cpp is not built (it needs nlohmann/json, an external library); the
+// harness only references write_csv from the CSV writers, which the oracle
+// never calls.
+namespace hgnn {
+void write_csv(const std::string&, const std::vector<std::string>&,
+               const std::vector<std::vector<std::string>>&) {
+  throw IoError("write_csv is not available in the oracle build");
+}
+}  // namespace hgnn
+
+using namespace hgnn;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefGraph {
+  MeshConfig mc;
+  DistributedGraph dg;
+};
+
+// Per-rank recorded tensors of one MP-stack run.
+struct RankRecord {
+  Tensor2D x0, e0;                          // MP stack inputs (encoder outputs in ref_run)
+  std::vector<Tensor2D> x_in, e_in, a_sync, x_out, e_out;
+  Tensor2D dx_m, de_m;                      // MP stack output adjoints
+  std::vector<Tensor2D> dx_in, de_in;       // adjoints of each layer's inputs
+  std::vector<double> mp_grads;             // MP-layer grads, for_each order, rank-local
+  std::vector<double> all_grads;            // full-model grads (ref_run only), rank-local
+  Tensor2D y, dy;
+  double loss = 0.0;
+};
+
+struct RefRun {
+  std::vector<RankRecord> ranks;
+  double loss = 0.0;
+  double fwd_ms = 0.0, bwd_ms = 0.0;
+};
+
+ExchangeMode to_mode(int m) {
+  return m == 0 ? ExchangeMode::None : (m == 1 ? ExchangeMode::AllToAll : ExchangeMode::NeighborAllToAll);
+}
+
+GnnConfig make_cfg(int64_t H, int64_t M, int64_t k, int mode) {
+  GnnConfig c;
+  c.name = "oracle";
+  c.hidden_dim = H;
+  c.num_mp_layers = M;
+  c.mlp_hidden_layers = k;
+  c.mode = to_mode(mode);
+  return c;
+}
+
+// MP-layer tensors of a ModelParams / ModelGrads in for_each order
+// (model.cpp:130-133).
+template <class Fn>
+void for_each_mp(ModelParams& p, Fn fn) {
+  for (auto& layer : p.layers) {
+    layer.edge_update.p.for_each([&](const std::string&, Tensor2D& t) { fn(t); });
+    layer.node_update.p.for_each([&](const std::string&, Tensor2D& t) { fn(t); });
+  }
+}
+template <class Fn>
+void for_each_mp(ModelGrads& g, Fn fn) {
+  for (auto& layer : g.layers) {
+    layer.edge_update.for_each([&](const std::string&, Tensor2D& t) { fn(t); });
+    layer.node_update.for_each([&](const std::string&, Tensor2D& t) { fn(t); });
+  }
+}
+
+void load_mp_params(ModelParams& p, const double* flat) {
+  int64_t off = 0;
+  for_each_mp(p, [&](Tensor2D& t) {
+    std::memcpy(t.data(), flat + off, sizeof(double) * static_cast<size_t>(t.size()));
+    off += t.size();
+  });
+}
+
+Tensor2D from_ptr(const double* src, int64_t rows, int64_t cols) {
+  Tensor2D t(rows, cols);
+  if (src) std::memcpy(t.data(), src, sizeof(double) * static_cast<size_t>(rows * cols));
+  return t;
+}
+
+// MP stack forward (gnn_forward's layer loop, model.cpp:295-300) + backward
+// (gnn_backward's layer loop, model.cpp:411-415) with every boundary tensor
+// recorded. dx_m/de_m are the adjoints entering the last layer.
+void run_mp_stack(const ModelParams& params, const ReducedGraph& g, const HaloMap& h, RankComm& comm,
+                  RankRecord& rec, ModelGrads& grads, double* fwd_ms, double* bwd_ms,
+                  const std::function<void(const Tensor2D& x_final, Tensor2D& dx, Tensor2D& de)>& head) {
+  const GnnConfig& cfg = params.config;
+  const size_t M = params.layers.size();
+  rec.x_in.resize(M); rec.e_in.resize(M); rec.a_sync.resize(M); rec.x_out.resize(M); rec.e_out.resize(M);
+  rec.dx_in.resize(M); rec.de_in.resize(M);
+  ForwardTrace trace;
+  trace.layers.resize(M);
+  auto x = std::make_shared<const Tensor2D>(rec.x0);
+  auto e = std::make_shared<const Tensor2D>(rec.e0);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (size_t m = 0; m < M; ++m) {
+    auto [x2, e2] = nmp_layer_forward(params.layers[m], g, h, &comm, cfg.mode, x, e, &trace.layers[m]);
+    x = std::make_shared<const Tensor2D>(std::move(x2));
+    e = std::make_shared<const Tensor2D>(std::move(e2));
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  for (size_t m = 0; m < M; ++m) {
+    rec.x_in[m] = *trace.layers[m].x_in;
+    rec.e_in[m] = *trace.layers[m].e_in;
+    rec.a_sync[m] = trace.layers[m].a_sync;
+    rec.x_out[m] = m + 1 < M ? *trace.layers[m + 1].x_in : *x;
+    rec.e_out[m] = m + 1 < M ? *trace.layers[m + 1].e_in : *e;
+  }
+  Tensor2D dx = rec.dx_m, de = rec.de_m;
+  if (head) {
+    head(*x, dx, de);
+    rec.dx_m = dx;
+    rec.de_m = de;
+  }
+  const auto t2 = std::chrono::steady_clock::now();
+  for (int64_t m = static_cast<int64_t>(M) - 1; m >= 0; --m) {
+    nmp_layer_backward(params.layers[static_cast<size_t>(m)], grads.layers[static_cast<size_t>(m)], g, h,
+                       &comm, cfg.mode, trace.layers[static_cast<size_t>(m)], dx, de);
+    rec.dx_in[static_cast<size_t>(m)] = dx;
+    rec.de_in[static_cast<size_t>(m)] = de;
+  }
+  const auto t3 = std::chrono::steady_clock::now();
+  if (fwd_ms) *fwd_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  if (bwd_ms) *bwd_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
+  ModelGrads& gg = grads;
+  for_each_mp(gg, [&](Tensor2D& t) { rec.mp_grads.insert(rec.mp_grads.end(), t.data(), t.data() + t.size()); });
+}
+
+const Tensor2D* pick(const RankRecord& r, int what, int layer) {
+  switch (what) {
+    case 0: return &r.x0;
+    case 1: return &r.e0;
+    case 2: return &r.x_in.at(static_cast<size_t>(layer));
+    case 3: return &r.e_in.at(static_cast<size_t>(layer));
+    case 4: return &r.a_sync.at(static_cast<size_t>(layer));
+    case 5: return &r.x_out.at(static_cast<size_t>(layer));
+    case 6: return &r.e_out.at(static_cast<size_t>(layer));
+    case 7: return &r.y;
+    case 8: return &r.dy;
+    case 9: return &r.dx_m;
+    case 10: return &r.dx_in.at(static_cast<size_t>(layer));
+    case 11: return &r.de_in.at(static_cast<size_t>(layer));
+    case 12: return &r.de_m;
+    default: return nullptr;
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// strategy: 0 slab, 1 block (factors fx,fy,fz if fx>0 else balanced_factors),
+// 2 = verify_partition (harness.cpp:42-45: slab at R=1, balanced block otherwise)
+void* ref_graph_build(int64_t E, int64_t p, int64_t R, int strategy, int64_t fx, int64_t fy, int64_t fz,
+                      int attach_features) {
+  RefGraph* rg = nullptr;
+  const int rc = guarded([&] {
+    auto owned = std::make_unique<RefGraph>();
+    owned->mc.elements_per_axis = E;
+    owned->mc.poly_order = p;
+    const Mesh mesh = build_box_mesh(owned->mc);
+    PartitionMap part;
+    if (strategy == 0) part = partition_mesh(mesh, R, PartitionStrategy::Slab);
+    else if (strategy == 1 && fx > 0) part = partition_mesh(mesh, R, PartitionStrategy::Block, {fx, fy, fz});
+    else if (strategy == 1) part = partition_mesh(mesh, R, PartitionStrategy::Block);
+    else part = verify_partition(mesh, R);
+    owned->dg = build_distributed_graph(mesh, part);
+    if (attach_features) attach_tgv_features(owned->dg, owned->mc);
+    rg = owned.release();
+  });
+  return rc == 0 ? rg : nullptr;
+}
+
+void ref_graph_free(void* h) { delete static_cast<RefGraph*>(h); }
+
+// out[0..8] = num_local, num_halo, num_edges, n_nbr, n_send_total, n_sync, n_sync_slots,
+//             max_buffer_rows, num_ranks
+void ref_graph_sizes(void* hnd, int rank, int64_t* out) {
+  const auto& rg = *static_cast<RefGraph*>(hnd);
+  const ReducedGraph& g = rg.dg.graphs.at(static_cast<size_t>(rank));
+  const HaloMap& h = rg.dg.halos.at(static_cast<size_t>(rank));
+  int64_t ns = 0, slots = 0;
+  for (const auto& m : h.send_masks) ns += static_cast<int64_t>(m.size());
+  for (const auto& grp : h.sync_groups) slots += static_cast<int64_t>(grp.slots.size());
+  out[0] = g.num_local;
+  out[1] = g.num_halo;
+  out[2] = g.num_edges();
+  out[3] = static_cast<int64_t>(h.neighbors.size());
+  out[4] = ns;
+  out[5] = static_cast<int64_t>(h.sync_groups.size());
+  out[6] = slots;
+  out[7] = h.max_buffer_rows;
+  out[8] = rg.dg.num_ranks();
+}
+
+void ref_graph_export(void* hnd, int rank, int64_t* gids, double* pos, double* node_feat, double* edge_feat,
+                      int32_t* src, int32_t* dst, int32_t* node_deg, int32_t* edge_deg, double* node_inv,
+                      double* edge_inv, int32_t* in_off, int32_t* in_edges, int32_t* out_off,
+                      int32_t* out_edges) {
+  const ReducedGraph& g = static_cast<RefGraph*>(hnd)->dg.graphs.at(static_cast<size_t>(rank));
+  auto cp = [](auto* dst_, const auto& v) {
+    if (dst_) std::memcpy(dst_, v.data(), sizeof(v[0]) * v.size());
+  };
+  cp(gids, g.global_ids);
+  if (pos) std::memcpy(pos, g.positions.data(), sizeof(double) * static_cast<size_t>(g.positions.size()));
+  if (node_feat && !g.node_features.empty())
+    std::memcpy(node_feat, g.node_features.data(), sizeof(double) * static_cast<size_t>(g.node_features.size()));
+  if (edge_feat && !g.edge_features.empty())
+    std::memcpy(edge_feat, g.edge_features.data(), sizeof(double) * static_cast<size_t>(g.edge_features.size()));
+  cp(src, g.edge_src);
+  cp(dst, g.edge_dst);
+  cp(node_deg, g.node_degree);
+  cp(edge_deg, g.edge_degree);
+  cp(node_inv, g.node_inv_degree);
+  cp(edge_inv, g.edge_inv_degree);
+  cp(in_off, g.in_offsets);
+  cp(in_edges, g.in_edges);
+  cp(out_off, g.out_offsets);
+  cp(out_edges, g.out_edges);
+}
+
+void ref_halo_export(void* hnd, int rank, int32_t* nbr, int32_t* send_off, int32_t* send_rows,
+                     int32_t* recv_off, int32_t* recv_rows, int32_t* halo_to_local, int32_t* sync_local,
+                     int32_t* sync_off, int32_t* sync_slots) {
+  const HaloMap& h = static_cast<RefGraph*>(hnd)->dg.halos.at(static_cast<size_t>(rank));
+  int32_t so = 0, ro = 0;
+  for (size_t n = 0; n < h.neighbors.size(); ++n) {
+    nbr[n] = h.neighbors[n];
+    send_off[n] = so;
+    recv_off[n] = ro;
+    for (int32_t v : h.send_masks[n]) send_rows[so++] = v;
+    for (int32_t v : h.recv_masks[n]) recv_rows[ro++] = v;
+  }
+  send_off[h.neighbors.size()] = so;
+  recv_off[h.neighbors.size()] = ro;
+  std::memcpy(halo_to_local, h.halo_to_local.data(), sizeof(int32_t) * h.halo_to_local.size());
+  int32_t go = 0;
+  for (size_t i = 0; i < h.sync_groups.size(); ++i) {
+    sync_local[i] = h.sync_groups[i].local_node;
+    sync_off[i] = go;
+    for (int32_t s : h.sync_groups[i].slots) sync_slots[go++] = s;
+  }
+  sync_off[h.sync_groups.size()] = go;
+}
+
+int64_t ref_param_count(int64_t H, int64_t M, int64_t k) {
+  return param_count(init_params(make_cfg(H, M, k, 2), 0));
+}
+
+int64_t ref_mp_param_count(int64_t H, int64_t M, int64_t k) {
+  ModelParams p = init_params(make_cfg(H, M, k, 2), 0);
+  int64_t n = 0;
+  for_each_mp(p, [&](Tensor2D& t) { n += t.size(); });
+  return n;
+}
+
+// Full model parameters in ModelParams::for_each order (model.cpp:124-135).
+void ref_init_params(int64_t H, int64_t M, int64_t k, uint64_t seed, double* flat) {
+  const ModelParams p = init_params(make_cfg(H, M, k, 2), seed);
+  int64_t off = 0;
+  p.for_each([&](const std::string&, const Tensor2D& t) {
+    std::memcpy(flat + off, t.data(), sizeof(double) * static_cast<size_t>(t.size()));
+    off += t.size();
+  });
+}
+
+// MP stack on caller-supplied inputs. mp_params: MP-layer tensors only, for_each order.
+// x0[r]: rows x H, e0[r]: N_e x H, dx_m[r]: rows x H, de_m[r] (nullable): N_e x H.
+void* ref_mp_run(void* graph, int64_t H, int64_t M, int64_t k, int mode, const double* mp_params,
+                 const double* const* x0, const double* const* e0, const double* const* dx_m,
+                 const double* const* de_m, int threads_per_rank) {
+  RefRun* out = nullptr;
+  const int rc = guarded([&] {
+    const DistributedGraph& dg = static_cast<RefGraph*>(graph)->dg;
+    ModelParams params = init_params(make_cfg(H, M, k, mode), 0);
+    load_mp_params(params, mp_params);
+    auto run = std::make_unique<RefRun>();
+    const int64_t R = dg.num_ranks();
+    run->ranks.resize(static_cast<size_t>(R));
+    std::vector<double> fwd(static_cast<size_t>(R)), bwd(static_cast<size_t>(R));
+    RankRuntime rt(R, threads_per_rank);
+    rt.run([&](RankComm& comm) {
+      const size_t r = static_cast<size_t>(comm.rank());
+      const ReducedGraph& g = dg.graphs[r];
+      RankRecord& rec = run->ranks[r];
+      rec.x0 = from_ptr(x0[r], g.rows(), H);
+      rec.e0 = from_ptr(e0[r], g.num_edges(), H);
+      rec.dx_m = from_ptr(dx_m[r], g.rows(), H);
+      rec.de_m = from_ptr(de_m ? de_m[r] : nullptr, g.num_edges(), H);
+      ModelGrads grads = make_grads(params);
+      run_mp_stack(params, g, dg.halos[r], comm, rec, grads, &fwd[r], &bwd[r], nullptr);
+    });
+    for (int64_t r = 0; r < R; ++r) {
+      run->fwd_ms = std::max(run->fwd_ms, fwd[static_cast<size_t>(r)]);
+      run->bwd_ms = std::max(run->bwd_ms, bwd[static_cast<size_t>(r)]);
+    }
+    out = run.release();
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+// Full compute_gradients pipeline (model.cpp:561-572) on the graph's TGV
+// features with init_params(seed) (or the supplied full parameter vector),
+// autoencoding target (model.cpp:605-607). Records the MP-stack boundary.
+void* ref_run(void* graph, int64_t H, int64_t M, int64_t k, int mode, uint64_t seed, const double* params_flat,
+              int threads_per_rank) {
+  RefRun* out = nullptr;
+  const int rc = guarded([&] {
+    const DistributedGraph& dg = static_cast<RefGraph*>(graph)->dg;
+    ModelParams params = init_params(make_cfg(H, M, k, mode), seed);
+    if (params_flat) {
+      int64_t off = 0;
+      params.for_each([&](const std::string&, Tensor2D& t) {
+        std::memcpy(t.data(), params_flat + off, sizeof(double) * static_cast<size_t>(t.size()));
+        off += t.size();
+      });
+    }
+    auto run = std::make_unique<RefRun>();
+    const int64_t R = dg.num_ranks();
+    run->ranks.resize(static_cast<size_t>(R));
+    std::vector<double> fwd(static_cast<size_t>(R)), bwd(static_cast<size_t>(R));
+    RankRuntime rt(R, threads_per_rank);
+    rt.run([&](RankComm& comm) {
+      const size_t r = static_cast<size_t>(comm.rank());
+      const ReducedGraph& g = dg.graphs[r];
+      const HaloMap& h = dg.halos[r];
+      RankRecord& rec = run->ranks[r];
+      auto [x0, e0] = encode(params, g.node_features, g.edge_features);
+      rec.x0 = x0;
+      rec.e0 = e0;
+      ModelGrads grads = make_grads(params);
+      Tensor2D target = local_rows(g.node_features, g.num_local);
+      auto head = [&](const Tensor2D& x_final, Tensor2D& dx, Tensor2D& de) {
+        // gnn_forward decode (model.cpp:303-306) + consistent loss + backward
+        // (model.cpp:565-567) + decoder backward (model.cpp:402-409).
+        Tensor2D y;
+        mlp_forward_rows(params.node_decoder, g.num_local, tensor_filler(x_final), y);
+        const ConsistentLoss loss = consistent_loss(comm, y, target, g.node_inv_degree);
+        const Tensor2D dy = consistent_loss_backward(comm, y, target, g.node_inv_degree, loss.n_eff);
+        dx = Tensor2D(g.rows(), H);
+        de = Tensor2D(g.num_edges(), H);
+        mlp_backward_rows(
+            params.node_decoder, g.num_local, tensor_filler(x_final), dy,
+            [&](int64_t row0, int64_t len, const double* d_in) {
+              std::memcpy(dx.row(row0), d_in, sizeof(double) * static_cast<size_t>(len * H));
+            },
+            grads.node_decoder);
+        rec.y = y;
+        rec.dy = dy;
+        rec.loss = loss.loss;
+      };
+      run_mp_stack(params, g, h, comm, rec, grads, &fwd[r], &bwd[r], head);
+      // encoders (model.cpp:417-423)
+      Tensor2D dx0 = rec.dx_in.empty() ? rec.dx_m : rec.dx_in.front();
+      Tensor2D de0 = rec.de_in.empty() ? rec.de_m : rec.de_in.front();
+      mlp_backward_rows(params.node_encoder, g.rows(), tensor_filler(g.node_features), dx0,
+                        [](int64_t, int64_t, const double*) {}, grads.node_encoder);
+      mlp_backward_rows(params.edge_encoder, g.num_edges(), tensor_filler(g.edge_features), de0,
+                        [](int64_t, int64_t, const double*) {}, grads.edge_encoder);
+      grads.for_each([&](const std::string&, Tensor2D& t) {
+        rec.all_grads.insert(rec.all_grads.end(), t.data(), t.data() + t.size());
+      });
+    });
+    run->loss = run->ranks[0].loss;
+    for (int64_t r = 0; r < R; ++r) {
+      run->fwd_ms = std::max(run->fwd_ms, fwd[static_cast<size_t>(r)]);
+      run->bwd_ms = std::max(run->bwd_ms, bwd[static_cast<size_t>(r)]);
+    }
+    out = run.release();
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void ref_run_free(void* run) { delete static_cast<RefRun*>(run); }
+double ref_run_loss(void* run) { return static_cast<RefRun*>(run)->loss; }
+void ref_run_times(void* run, double* fwd_ms, double* bwd_ms) {
+  *fwd_ms = static_cast<RefRun*>(run)->fwd_ms;
+  *bwd_ms = static_cast<RefRun*>(run)->bwd_ms;
+}
+
+// Number of doubles of an exported tensor (or -1 if absent).
+int64_t ref_run_size(void* run, int rank, int what, int layer) {
+  const RankRecord& r = static_cast<RefRun*>(run)->ranks.at(static_cast<size_t>(rank));
+  if (what == 13) return static_cast<int64_t>(r.mp_grads.size());
+  if (what == 14) return static_cast<int64_t>(r.all_grads.size());
+  const Tensor2D* t = pick(r, what, layer);
+  return t ? t->size() : -1;
+}
+
+void ref_run_export(void* run, int rank, int what, int layer, double* out) {
+  const RankRecord& r = static_cast<RefRun*>(run)->ranks.at(static_cast<size_t>(rank));
+  if (what == 13) {
+    std::memcpy(out, r.mp_grads.data(), sizeof(double) * r.mp_grads.size());
+    return;
+  }
+  if (what == 14) {
+    std::memcpy(out, r.all_grads.data(), sizeof(double) * r.all_grads.size());
+    return;
+  }
+  const Tensor2D* t = pick(r, what, layer);
+  std::memcpy(out, t->data(), sizeof(double) * static_cast<size_t>(t->size()));
+}
+
+}  // extern "C"

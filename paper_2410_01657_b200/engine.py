@@ -1,0 +1,149 @@
+"""Per-rank device engine: the B200 drop-in for the reference's MP stack.
+
+Mirrors the reference interface of the hot path (model.hpp:98-116):
+  Engine.nmp_forward   ~ gnn_forward's layer loop (M x nmp_layer_forward)
+  Engine.nmp_backward  ~ gnn_backward's layer loop (M x nmp_layer_backward)
+  Engine.trace         ~ NmpLayerTrace (x_in, e_in, a_sync) plus layer outputs
+One Engine per rank / GPU (one process per GPU under torchrun); ranks share an
+NCCL communicator whose unique id is broadcast by the caller.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .graph import RankGraph
+from .params import GnnConfig
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    N.check(N.LIB.hgnn_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _f64(a: np.ndarray | None, shape=None):
+    if a is None:
+        return None, None
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and a.shape != shape and a.size != int(np.prod(shape)):
+        raise N.ShapeError(f"expected shape {shape}, got {a.shape}")
+    return a, a.ctypes.data_as(N.f64p)
+
+
+class Engine:
+    def __init__(self, device: int = 0, rank: int = 0, num_ranks: int = 1, uid: bytes | None = None):
+        self._h = C.c_void_p()
+        uid_buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
+        N.check(N.LIB.hgnn_ctx_create(device, rank, num_ranks, uid_buf, C.byref(self._h)))
+        self.rank, self.num_ranks, self.device = rank, num_ranks, device
+        self.graph: RankGraph | None = None
+        self.cfg: GnnConfig | None = None
+
+    def close(self) -> None:
+        if self._h:
+            N.check(N.LIB.hgnn_ctx_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        return N.LIB.hgnn_ctx_stream(self._h) or 0
+
+    # ---- setup -----------------------------------------------------------
+    def upload_graph(self, g: RankGraph) -> None:
+        d = g.desc()
+        N.check(N.LIB.hgnn_graph_upload(self._h, C.byref(d)))
+        self.graph = g
+
+    def configure(self, cfg: GnnConfig) -> None:
+        N.check(N.LIB.hgnn_configure(self._h, cfg.hidden_dim, cfg.num_mp_layers, cfg.mlp_hidden_layers,
+                                     N.MODES[cfg.mode]))
+        self.cfg = cfg
+
+    def upload_params(self, mp_params: np.ndarray) -> None:
+        a, p = _f64(mp_params)
+        N.check(N.LIB.hgnn_params_upload(self._h, p, a.size))
+
+    # ---- MP stack ----------------------------------------------------------
+    def nmp_forward(self, x0: np.ndarray, e0: np.ndarray, want_e: bool = False):
+        """Runs the M consistent NMP layers; returns x_M (rows x H) [and e_M]."""
+        g, H = self.graph, self.cfg.hidden_dim
+        x, xp = _f64(x0, (g.rows, H))
+        e, ep = _f64(e0, (g.num_edges, H))
+        xo = np.empty((g.rows, H))
+        eo = np.empty((g.num_edges, H)) if want_e else None
+        N.check(N.LIB.hgnn_mp_forward(self._h, xp, ep, xo.ctypes.data_as(N.f64p),
+                                      eo.ctypes.data_as(N.f64p) if want_e else None))
+        return (xo, eo) if want_e else xo
+
+    def nmp_backward(self, dx: np.ndarray, de: np.ndarray | None = None):
+        """Adjoint of the MP stack; returns (dx0, de0, mp_grads)."""
+        g, H = self.graph, self.cfg.hidden_dim
+        d, dp = _f64(dx, (g.rows, H))
+        e, epp = _f64(de, (g.num_edges, H))
+        dx0 = np.empty((g.rows, H))
+        de0 = np.empty((g.num_edges, H))
+        n_par = self.cfg.num_mp_layers * (_mlp(3 * H, H, self.cfg.mlp_hidden_layers)
+                                          + _mlp(2 * H, H, self.cfg.mlp_hidden_layers))
+        grads = np.empty(n_par)
+        N.check(N.LIB.hgnn_mp_backward(self._h, dp, epp, dx0.ctypes.data_as(N.f64p), de0.ctypes.data_as(N.f64p),
+                                       grads.ctypes.data_as(N.f64p)))
+        return dx0, de0, grads
+
+    def trace(self, layer: int, which: str) -> np.ndarray:
+        g, H = self.graph, self.cfg.hidden_dim
+        sel = {"x_in": N.TRACE_X_IN, "e_in": N.TRACE_E_IN, "a_sync": N.TRACE_A_SYNC, "x_out": N.TRACE_X_OUT,
+               "e_out": N.TRACE_E_OUT}[which]
+        n = g.num_edges if which.startswith("e") else g.rows
+        out = np.empty((n, H))
+        N.check(N.LIB.hgnn_get_trace(self._h, layer, sel, out.ctypes.data_as(N.f64p)))
+        return out
+
+    # ---- device-resident step (benchmark) ---------------------------------
+    def synthetic_inputs(self, seed: int = 0) -> None:
+        N.check(N.LIB.hgnn_synthetic_inputs(self._h, seed))
+
+    def set_inputs(self, x0, e0, dx) -> None:
+        _, xp = _f64(x0)
+        _, ep = _f64(e0)
+        _, dp = _f64(dx)
+        N.check(N.LIB.hgnn_set_inputs(self._h, xp, ep, dp))
+
+    def step_device(self) -> None:
+        N.check(N.LIB.hgnn_mp_step_device(self._h))
+
+    def grads(self) -> np.ndarray:
+        H, k = self.cfg.hidden_dim, self.cfg.mlp_hidden_layers
+        out = np.empty(self.cfg.num_mp_layers * (_mlp(3 * H, H, k) + _mlp(2 * H, H, k)))
+        N.check(N.LIB.hgnn_get_grads(self._h, out.ctypes.data_as(N.f64p)))
+        return out
+
+    # ---- instrumentation ---------------------------------------------------
+    def kernel_timing(self, enable: bool) -> None:
+        N.check(N.LIB.hgnn_kernel_timing(self._h, int(enable)))
+
+    def kernel_times(self) -> dict[str, tuple[float, int]]:
+        out = {}
+        for i, name in enumerate(N.KERNEL_CLASSES):
+            t, n = C.c_double(), C.c_int64()
+            N.check(N.LIB.hgnn_kernel_time(self._h, i, C.byref(t), C.byref(n)))
+            out[name] = (t.value, n.value)
+        return out
+
+    def launch_count(self, reset: bool = False) -> int:
+        return N.LIB.hgnn_launch_count(self._h, int(reset))
+
+    def halo_bytes(self, reset: bool = False) -> int:
+        return N.LIB.hgnn_halo_bytes(self._h, int(reset))
+
+
+def _mlp(in_dim: int, H: int, k: int) -> int:
+    return in_dim * H + H + k * (H * H + H) + H * H + H
