@@ -1,0 +1,382 @@
+"""Benchmark: consistent MP-layer stack (forward + backward) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU)
+
+Workload (BASELINE.json configs[2] at N=1): 32^3-element GLL box at P=5
+(4,173,281 nodes, 24,884,160 directed edges), hidden 64, 5 hidden blocks per
+MLP, 4 MP layers, exchange mode na2a. N>1 runs the weak-scaling series of
+configs[4] (~4.2M nodes per GPU: E = 40/50/64 at N = 2/4/8, balanced block
+partition), one GPU per rank, NCCL halo exchange over NVLink.
+
+metric: MP-layer graph nodes per second, fwd+bwd
+        = (unique global nodes) x (MP layers) / (time of one MP-stack fwd+bwd step)
+value: device-resident inputs (synthetic, keyed by global id), CUDA events on
+       the engine stream, max over ranks.
+e2e:   same metric through the public C-ABI with fp64 host buffers in the
+       reference layout (x0, e0, dx_M H2D; parameter gradients D2H) per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+LOADING = 4_173_281  # configs[2] nodes per GPU
+P_ORDER, HIDDEN, M_LAYERS, K_HIDDEN = 5, 64, 4, 5
+METRIC = "MP-layer graph nodes/sec (fwd+bwd)"
+UNIT = "layer-nodes/s"
+
+
+def choose_elements_for_loading(ranks: int, loading: int, p: int) -> int:
+    """harness.cpp:271-296 (mesh sizing rule of the reference weak-scaling harness)."""
+    from paper_2410_01657_b200 import PartitionError, balanced_factors
+    best, best_err = -1, 0.0
+    for e in range(1, 97):
+        feasible = e % ranks == 0 and ranks <= e
+        if not feasible:
+            try:
+                balanced_factors(ranks, e)
+                feasible = True
+            except PartitionError:
+                feasible = False
+        if not feasible:
+            continue
+        per_rank = (e * p + 1) ** 3 / ranks
+        err = abs(per_rank - loading)
+        if best < 0 or err < best_err:
+            best, best_err = e, err
+    return best
+
+
+def workload(n_gpus: int):
+    E = 32 if n_gpus == 1 else choose_elements_for_loading(n_gpus, LOADING, P_ORDER)
+    return {"E": E, "p": P_ORDER, "H": HIDDEN, "M": M_LAYERS, "k": K_HIDDEN, "mode": "na2a",
+            "unique_nodes": (E * P_ORDER + 1) ** 3}
+
+
+def edge_flops(H, k):
+    return 2 * H * H * (4 + k)
+
+
+def node_flops(H, k):
+    return 2 * H * H * (3 + k)
+
+
+# --------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# --------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [t.strip() for t in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        under_load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(under_load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# CPU reference timing (oracle/_ref = the reference compiled in place; else the
+# C restatement). Test infrastructure: only this leg executes oracle/.
+# --------------------------------------------------------------------------
+def cpu_reference_sample(steps: int = 1, E: int = 5):
+    import oracle as O
+    H, M, k = HIDDEN, 1, K_HIDDEN
+    from paper_2410_01657_b200 import GnnConfig, build_rank_graph, init_params, mp_params
+    cfg = GnnConfig("bench", H, M, k, mode="na2a")
+    mp = mp_params(cfg, init_params(cfg, 0))
+    rng = np.random.default_rng(0)
+    nodes = (E * P_ORDER + 1) ** 3
+    cores = os.cpu_count() or 1
+    times = []
+    if O.ref_available():
+        kind = "reference"
+        g = O.RefGraph(E, P_ORDER, 1, "verify", features=False)
+        rg = g.ranks[0]
+        x0 = [rng.uniform(-1, 1, (rg.num_local + rg.num_halo, H))]
+        e0 = [rng.uniform(-1, 1, (rg.num_edges, H))]
+        dx = [rng.uniform(-1e-2, 1e-2, (rg.num_local + rg.num_halo, H))]
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            run = O.ref_mp_run(g, H, M, k, "na2a", mp, x0, e0, dx)
+            times.append(time.perf_counter() - t0)
+            del run
+    else:
+        kind = "port"
+        cores = 1
+        rg = build_rank_graph(E, P_ORDER, 1, 0, "verify")
+        x0 = [rng.uniform(-1, 1, (rg.rows, H))]
+        e0 = [rng.uniform(-1, 1, (rg.num_edges, H))]
+        dx = [rng.uniform(-1e-2, 1e-2, (rg.rows, H))]
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.oracle_mp_run([rg], H, M, k, "na2a", mp, x0, e0, dx)
+            times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": nodes * M / t, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"1 MP layer fwd+bwd (fp64, OpenMP over all host threads), {E}^3-element box at P={P_ORDER} "
+                      f"({nodes} nodes), H={H}, k={k}, R=1; median of {len(times)} run(s), {t:.2f} s each",
+            "seconds": t}
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    n = a.gpus
+    wl = workload(n)
+    if rank != 0:
+        return
+    for _ in range(a.warmup if a.warmup < 2 else 1):
+        cpu_reference_sample(1, a.ref_elements)
+    res = cpu_reference_sample(max(1, a.steps), a.ref_elements)
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": n,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(wl, n), "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind",
+                                                                                 "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(wl, n):
+    return {"workload": f"consistent MP stack fwd+bwd, {wl['E']}^3-element GLL box P={wl['p']} "
+                        f"({wl['unique_nodes']} nodes), H={wl['H']}, k={wl['k']}, M={wl['M']}, mode={wl['mode']}",
+            "elements_per_axis": wl["E"], "poly_order": wl["p"], "hidden": wl["H"], "mlp_hidden_layers": wl["k"],
+            "mp_layers": wl["M"], "mode": wl["mode"], "unique_nodes": wl["unique_nodes"],
+            "partition": "single rank" if n == 1 else "balanced block (verify_partition, harness.cpp:42-45)",
+            "parallelism": f"domain decomposition x{n}", "l2": "inputs larger than L2 (no flush needed)"}
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-elements", type=int, default=5)
+    ap.add_argument("--elements", type=int, default=0, help="override E (debug)")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline / clocks")
+    a = ap.parse_args()
+    if a.impl == "reference":
+        run_reference_arm(a)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_01657_b200 import Engine, GnnConfig, build_rank_graph, init_params, mp_params, nccl_unique_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = a.gpus
+    if world != n:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl = workload(n)
+    if a.elements:
+        wl["E"] = a.elements
+        wl["unique_nodes"] = (a.elements * P_ORDER + 1) ** 3
+    H, M, k = wl["H"], wl["M"], wl["k"]
+
+    uid = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    torch.cuda.set_device(local)
+    t0 = time.time()
+    g = build_rank_graph(wl["E"], wl["p"], n, rank, "verify")
+    t_graph = time.time() - t0
+    cfg = GnnConfig("bench", H, M, k, mode=wl["mode"])
+    eng = Engine(local, rank, n, uid)
+    eng.upload_graph(g)
+    eng.configure(cfg)
+    eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+    eng.synthetic_inputs(seed=1234)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        eng.step_device()
+    barrier()
+    clocks = Clocks(local) if not a.profile else None
+    eng.kernel_timing(True)
+    eng.launch_count(reset=True)
+    eng.halo_bytes(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    for _ in range(a.steps):
+        eng.step_device()
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    launches = eng.launch_count() // a.steps
+    ktimes = eng.kernel_times()
+    halo_bytes = eng.halo_bytes() // a.steps
+    eng.kernel_timing(False)
+    clk = clocks.stop() if clocks else None
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = wl["unique_nodes"] * M / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel class (live CUDA-event durations)
+    per_launch = {c: (t / max(nl_, 1), nl_) for c, (t, nl_) in ktimes.items()}
+    step_share = {c: t / a.steps / ms for c, (t, _) in ktimes.items()}
+    flops = {"edge_bwd": g.num_edges * 2 * edge_flops(H, k), "edge_fwd": g.num_edges * edge_flops(H, k),
+             "node_bwd": g.num_local * 2 * node_flops(H, k), "node_fwd": g.num_local * node_flops(H, k)}
+    dom = max(flops, key=lambda c: ktimes[c][0])
+    peaks = json.load(open(ROOT / "MEASURED_PEAKS.json")) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    bf16 = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1590.0
+    tf32_peak = bf16 / 2.0
+    avg_ms = per_launch[dom][0]
+    achieved = flops[dom] / (avg_ms / 1e3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.load(open(prof)).get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": achieved / tf32_peak, "traffic": traffic, "kernel": dom,
+                "peak_basis": "dense TF32 = 1/2 of measured sustained bf16 (MEASURED_PEAKS.json)",
+                "flops_per_launch": flops[dom], "ms_per_launch": avg_ms,
+                "pipe": "fp32 SIMT (v1 kernels; tcgen05 path pending)"}
+
+    # ---- e2e through the public C-ABI with host buffers
+    e2e = None
+    if not a.no_e2e and not a.profile:
+        e2e = run_e2e(a, eng, g, cfg, stream, barrier, world, dist, torch, wl)
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and n == 1 and not a.no_cpu_baseline and not a.profile:
+        try:
+            res = cpu_reference_sample(1, a.ref_elements)
+            cpu = {k2: res[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": a.steps, "warmup": a.warmup,
+                "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (seeded by global id; random-init weights init_params seed 0)",
+                "config": config_dict(wl, n), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+                "cpu_baseline": cpu, "clocks": clk,
+                "kernel_share": {c: round(v, 4) for c, v in step_share.items()},
+                "halo_share": round(step_share.get("halo", 0.0), 4), "halo_bytes_per_step_rank0": halo_bytes,
+                "graph_build_s": round(t_graph, 3),
+                "nodes_per_sec_per_iteration": wl["unique_nodes"] / (ms_max / 1e3)}
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, eng, g, cfg, stream, barrier, world, dist, torch, wl):
+    H = cfg.hidden_dim
+    rows, ne = g.rows, g.num_edges
+
+    def pinned(shape):
+        try:
+            t = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+            return t.numpy(), True
+        except Exception:
+            return np.empty(shape, dtype=np.float64), False
+
+    x0, p1 = pinned((rows, H))
+    e0, p2 = pinned((ne, H))
+    dx, p3 = pinned((rows, H))
+    rng = np.random.default_rng(5)
+    blk = rng.uniform(-1, 1, (4096, H))
+    for arr in (x0, e0, dx):
+        for o in range(0, arr.shape[0], 4096):
+            m = min(4096, arr.shape[0] - o)
+            arr[o:o + m] = blk[:m]
+    dx *= 1e-3
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.nmp_forward(x0, e0)  # warm-up (allocations, page-in)
+    eng.nmp_backward(dx)
+    barrier()
+    ev0.record(stream)
+    for _ in range(a.e2e_steps):
+        eng.nmp_forward(x0, e0)
+        eng.nmp_backward(dx)
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1) / a.e2e_steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_par = len(eng.grads())
+    return {"value": wl["unique_nodes"] * cfg.num_mp_layers / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": int((2 * rows + ne) * H * 8), "d2h_bytes_per_step": int(n_par * 8),
+            "ms_per_step": ms, "pinned": bool(p1 and p2 and p3), "steps": a.e2e_steps,
+            "api": "hgnn_mp_forward + hgnn_mp_backward (fp64 host, reference edge-id order)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,62 @@
+"""One rank of a multi-GPU parity run (launched by test_gpu_multirank.py).
+
+Inputs are functions of global ids only, so coincident nodes / duplicated
+edges carry identical values on every rank, as in the reference harness.
+"""
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2410_01657_b200 import Engine, GnnConfig, build_rank_graph, init_params, mp_params  # noqa: E402
+
+
+def gid_inputs(g, H):
+    cols = np.arange(H)[None, :]
+    x0 = np.sin(0.37 * g.global_ids[:, None] + 0.5 * cols)
+    key = (g.global_ids[g.edge_src] * 7919 + g.global_ids[g.edge_dst]).astype(np.float64)
+    e0 = np.cos(1e-3 * key[:, None] + 0.3 * cols)
+    dx = 1e-2 * np.cos(0.21 * g.global_ids[:, None] - 0.7 * cols)
+    # consistent output adjoint: coincident copies carry 1/d of the seed
+    # (consistent_loss_backward, model.cpp:493-499)
+    dx[:g.num_local] *= g.node_inv_degree[:, None]
+    dx[g.num_local:] = 0.0
+    return x0, e0, dx
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rank", type=int)
+    ap.add_argument("--R", type=int)
+    ap.add_argument("--uid")
+    ap.add_argument("--E", type=int)
+    ap.add_argument("--p", type=int)
+    ap.add_argument("--H", type=int)
+    ap.add_argument("--M", type=int)
+    ap.add_argument("--k", type=int)
+    ap.add_argument("--mode")
+    ap.add_argument("--out")
+    a = ap.parse_args()
+    cfg = GnnConfig("w", a.H, a.M, a.k, mode=a.mode)
+    g = build_rank_graph(a.E, a.p, a.R, a.rank, "verify")
+    eng = Engine(a.rank, a.rank, a.R, bytes.fromhex(a.uid))
+    eng.upload_graph(g)
+    eng.configure(cfg)
+    eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+    x0, e0, dx = gid_inputs(g, a.H)
+    x_out, e_out = eng.nmp_forward(x0, e0, want_e=True)
+    a_sync0 = eng.trace(0, "a_sync")
+    dx0, de0, grads = eng.nmp_backward(dx)
+    x_out2 = eng.nmp_forward(x0, e0)
+    np.savez(a.out, x_out=x_out, e_out=e_out, a_sync0=a_sync0, dx0=dx0, de0=de0, grads=grads, x_out2=x_out2,
+             halo_bytes=eng.halo_bytes())
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
