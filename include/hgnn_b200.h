@@ -108,6 +108,9 @@ int hgnn_mp_param_range(int64_t hidden, int64_t num_mp_layers, int64_t mlp_hidde
 /* ========================================================================== */
 typedef struct hgnn_ctx hgnn_ctx;
 
+/* Number of visible CUDA devices (0 when no driver / GPU is present). */
+int hgnn_device_count(void);
+
 /* NCCL unique id (128 bytes) created on rank 0 and broadcast by the caller. */
 int hgnn_nccl_unique_id(uint8_t out[128]);
 

@@ -84,7 +84,7 @@ class GraphDesc(C.Structure):
 def _load() -> C.CDLL:
     if not _LIB_PATH.exists():
         raise ImportError(
-            f"{_LIB_PATH} is missing: build it with `python -m paper_2410_01657_b200.build` "
+            f"{_LIB_PATH} is missing: build it with `python paper_2410_01657_b200/build.py` "
             "(the hot path has no CPU fallback)")
     lib = C.CDLL(str(_LIB_PATH), mode=C.RTLD_GLOBAL)
     vp, u8p = C.c_void_p, C.POINTER(C.c_uint8)
@@ -97,6 +97,7 @@ def _load() -> C.CDLL:
         "hgnn_param_count": (C.c_int64, [C.c_int64] * 6),
         "hgnn_init_params": (C.c_int, [C.c_int64] * 6 + [C.c_uint64, f64p]),
         "hgnn_mp_param_range": (C.c_int, [C.c_int64] * 5 + [i64p, i64p]),
+        "hgnn_device_count": (C.c_int, []),
         "hgnn_nccl_unique_id": (C.c_int, [u8p]),
         "hgnn_ctx_create": (C.c_int, [C.c_int, C.c_int32, C.c_int32, u8p, C.POINTER(vp)]),
         "hgnn_ctx_destroy": (C.c_int, [vp]),
@@ -125,7 +126,7 @@ def _load() -> C.CDLL:
 
 LIB = _load()
 EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_graph_view", "hgnn_balanced_factors",
-            "hgnn_param_count", "hgnn_init_params", "hgnn_mp_param_range", "hgnn_nccl_unique_id",
+            "hgnn_param_count", "hgnn_init_params", "hgnn_mp_param_range", "hgnn_device_count", "hgnn_nccl_unique_id",
             "hgnn_ctx_create", "hgnn_ctx_destroy", "hgnn_ctx_stream", "hgnn_graph_upload", "hgnn_configure",
             "hgnn_params_upload", "hgnn_mp_forward", "hgnn_mp_backward", "hgnn_get_trace",
             "hgnn_synthetic_inputs", "hgnn_set_inputs", "hgnn_mp_step_device", "hgnn_get_grads",

@@ -1,7 +1,8 @@
 """In-tree build of the native library (sm_100a) and of the test oracle.
 
-    python -m paper_2410_01657_b200.build            # product .so
-    python -m paper_2410_01657_b200.build --oracle   # + oracle/_build and oracle/_ref
+    python paper_2410_01657_b200/build.py            # product .so
+    python paper_2410_01657_b200/build.py --oracle   # + oracle/_build and oracle/_ref
+(run by path: importing the package would first load the native library)
 
 The product library `paper_2410_01657_b200/lib/libhgnn_b200.so` is compiled
 directly with nvcc for `-gencode arch=compute_100a,code=sm_100a` (no JIT, no

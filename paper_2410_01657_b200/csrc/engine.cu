@@ -564,6 +564,15 @@ void require_ready(hgnn_ctx* c) {
 // ==========================================================================
 extern "C" {
 
+int hgnn_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 int hgnn_nccl_unique_id(uint8_t out[128]) {
   return guarded([&] {
     static_assert(sizeof(ncclUniqueId) == 128, "unexpected ncclUniqueId size");

@@ -27,7 +27,10 @@ def pytest_configure(config):
     lib = ROOT / "paper_2410_01657_b200" / "lib" / "libhgnn_b200.so"
     orc = ROOT / "oracle" / "_build" / "liboracle.so"
     if not lib.exists() or not orc.exists():
-        from paper_2410_01657_b200 import build as B  # noqa: WPS433
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("hgnn_b200_build", ROOT / "paper_2410_01657_b200" / "build.py")
+        B = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(B)
         if not lib.exists():
             B.build_library()
         if not orc.exists():
@@ -35,11 +38,8 @@ def pytest_configure(config):
 
 
 def gpu_count() -> int:
-    try:
-        import torch
-        return torch.cuda.device_count()
-    except Exception:
-        return 0
+    from paper_2410_01657_b200 import _native as N
+    return N.LIB.hgnn_device_count()
 
 
 @pytest.fixture(scope="session")
