@@ -161,6 +161,11 @@ int hgnn_mp_step_device(hgnn_ctx* ctx);
 /* Device gradients -> host (fp64), same layout as hgnn_params_upload. */
 int hgnn_get_grads(hgnn_ctx* ctx, double* mp_grads);
 
+/* ---- options --------------------------------------------------------------- */
+/* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
+ *                     0 = SIMT fp32 kernels. */
+int hgnn_set_option(hgnn_ctx* ctx, const char* key, int64_t value);
+
 /* ---- instrumentation ------------------------------------------------------ */
 /* When enabled, every launch of the listed kernel classes is bracketed by CUDA
  * events on its stream; totals are read back with hgnn_kernel_time. */

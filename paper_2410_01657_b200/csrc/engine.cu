@@ -20,6 +20,7 @@
 #include "common.hpp"
 #include "graph_kernels.cuh"
 #include "mlp_simt.cuh"
+#include "mlp_tc.cuh"
 
 using namespace hgnn_b200;
 
@@ -96,7 +97,10 @@ struct hgnn_ctx {
   // parameters (fp32) and gradients (fp64), MP layers
   int64_t n_edge_par = 0, n_node_par = 0, n_mp_par = 0;
   DevBuf<float> par, par_t;
+  DevBuf<float> chunks;                 // tcgen05 B operands, [W_hi | W_lo]^T chunks per MLP
+  std::vector<int64_t> chunk_off;       // per (layer, edge/node)
   DevBuf<double> grads;
+  int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
 
   // activations
   std::vector<std::unique_ptr<DevBuf<float>>> xs, es, as;
@@ -221,6 +225,45 @@ void launch_mlp(hgnn_ctx* c, bool forward, int mode, const MlpRowArgs& args, con
   void* params[] = {&a, &p};
   CUDA_OK(cudaLaunchKernel(k, dim3(grid), dim3(kMlpThreads), params, smem, c->stream));
   check_launch(c);
+}
+
+// --------------------------------------------------------------------------
+// tcgen05 weight chunks (host-side layout, mlp_tc.cuh)
+// --------------------------------------------------------------------------
+float tf32_rna_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+bool tc_eligible(const hgnn_ctx* c) { return c->H == 32 || c->H == 64; }
+
+// Chunks of one processor MLP in MMA order: the input linear split into
+// nseg K-chunks of H rows, then one chunk per H x H linear. Each chunk is the
+// B operand [W_hi | W_lo]^T (2H x H) in K-major core-matrix order.
+void build_chunks(const float* p, int in_dim, int H, int K, std::vector<float>& out) {
+  const int nseg = in_dim / H;
+  for (int l = 0; l < K + 2; ++l) {
+    const float* W = p + mlp_w_offset(l, in_dim, H);
+    const int n_ch = l == 0 ? nseg : 1;
+    for (int cidx = 0; cidx < n_ch; ++cidx) {
+      const size_t base = out.size();
+      out.resize(base + (size_t)2 * H * H);
+      for (int kk = 0; kk < H; ++kk) {
+        const int row = cidx * H + kk;
+        for (int n = 0; n < H; ++n) {
+          const float w = W[(int64_t)row * H + n];
+          const float hi = tf32_rna_host(w);
+          const float lo = tf32_rna_host(w - hi);
+          out[base + (size_t)tc_chunk_index(n, kk, H)] = hi;
+          out[base + (size_t)tc_chunk_index(H + n, kk, H)] = lo;
+        }
+      }
+    }
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -424,6 +467,47 @@ MlpParamsDev layer_params(hgnn_ctx* c, int64_t m, bool edge) {
   return p;
 }
 
+bool use_tc(const hgnn_ctx* c) { return c->fwd_impl == 1 && tc_eligible(c); }
+
+template <int H, int MODE>
+void launch_tc_typed(hgnn_ctx* c, const TcFwdArgs& args) {
+  using Cfg = TcCfg<H>;
+  auto k = mlp_tc_forward_kernel<H, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    attr = true;
+  }
+  const int64_t pairs = ((args.n_rows + 127) / 128 + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM, c->stream>>>(args);
+  check_launch(c);
+}
+
+void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const float* x, const float* e,
+                       const float* a, float* out) {
+  if (n_rows == 0) return;
+  const bool edge = mode == kEdgeInput;
+  TcFwdArgs args{};
+  args.n_rows = n_rows;
+  args.src = c->src.p;
+  args.dst = c->dst.p;
+  args.x = x;
+  args.e_in = e;
+  args.a = a;
+  args.out = out;
+  args.chunks = c->chunks.p + c->chunk_off[(size_t)(2 * m + (edge ? 0 : 1))];
+  args.params = layer_params(c, m, edge).p;
+  args.k = (int)c->K;
+  if (c->H == 64) {
+    if (edge) launch_tc_typed<64, kEdgeInput>(c, args);
+    else launch_tc_typed<64, kNodeInput>(c, args);
+  } else {
+    if (edge) launch_tc_typed<32, kEdgeInput>(c, args);
+    else launch_tc_typed<32, kNodeInput>(c, args);
+  }
+}
+
 void layer_forward(hgnn_ctx* c, int64_t m) {
   const int64_t H = c->H;
   float* x = c->xs[m]->p;
@@ -433,14 +517,18 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   float* x2 = c->xs[m + 1]->p;
   {  // edge update (model.cpp:233-235)
     Timed t(c, HGNN_K_EDGE_FWD);
-    MlpRowArgs args{};
-    args.n_rows = c->ne;
-    args.src = c->src.p;
-    args.dst = c->dst.p;
-    args.x = x;
-    args.e_in = e;
-    args.out = e2;
-    launch_mlp(c, true, kEdgeInput, args, layer_params(c, m, true));
+    if (use_tc(c)) {
+      launch_tc_forward(c, kEdgeInput, m, c->ne, x, e, nullptr, e2);
+    } else {
+      MlpRowArgs args{};
+      args.n_rows = c->ne;
+      args.src = c->src.p;
+      args.dst = c->dst.p;
+      args.x = x;
+      args.e_in = e;
+      args.out = e2;
+      launch_mlp(c, true, kEdgeInput, args, layer_params(c, m, true));
+    }
   }
   {  // degree-scaled aggregation (model.cpp:237-240)
     Timed t(c, HGNN_K_AGG);
@@ -460,12 +548,16 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   {  // node update on local rows (model.cpp:260-264)
     Timed t(c, HGNN_K_NODE_FWD);
     if (c->nh > 0) CUDA_OK(cudaMemsetAsync(x2 + c->nl * H, 0, sizeof(float) * (size_t)(c->nh * H), c->stream));
-    MlpRowArgs args{};
-    args.n_rows = c->nl;
-    args.x = x;
-    args.a = a;
-    args.out = x2;
-    launch_mlp(c, true, kNodeInput, args, layer_params(c, m, false));
+    if (use_tc(c)) {
+      launch_tc_forward(c, kNodeInput, m, c->nl, x, nullptr, a, x2);
+    } else {
+      MlpRowArgs args{};
+      args.n_rows = c->nl;
+      args.x = x;
+      args.a = a;
+      args.out = x2;
+      launch_mlp(c, true, kNodeInput, args, layer_params(c, m, false));
+    }
   }
 }
 
@@ -798,6 +890,19 @@ int hgnn_params_upload(hgnn_ctx* c, const double* flat, int64_t count) {
       }
     c->par.upload(p.data(), count, c->stream);
     c->par_t.upload(pt.data(), count, c->stream);
+    if (tc_eligible(c)) {
+      std::vector<float> ch;
+      c->chunk_off.clear();
+      int64_t poff = 0;
+      for (int64_t m = 0; m < c->M; ++m)
+        for (int which = 0; which < 2; ++which) {
+          const int in_dim = (which == 0 ? 3 : 2) * H;
+          c->chunk_off.push_back((int64_t)ch.size());
+          build_chunks(p.data() + poff, in_dim, H, K, ch);
+          poff += mlp_param_count(in_dim, H, K);
+        }
+      c->chunks.upload(ch.data(), (int64_t)ch.size(), c->stream);
+    }
     c->grads.alloc(std::max<int64_t>(count, 1));
     CUDA_OK(cudaStreamSynchronize(c->stream));
     c->params_ready = true;
@@ -907,6 +1012,19 @@ int hgnn_get_grads(hgnn_ctx* c, double* out) {
     if (!c->params_ready) fail(HGNN_ERR_UNINITIALIZED, "no parameters");
     CUDA_OK(cudaMemcpyAsync(out, c->grads.p, sizeof(double) * (size_t)c->n_mp_par, cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
+  return guarded([&] {
+    bind(c);
+    const std::string k = key ? key : "";
+    if (k == "mlp_forward_impl") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_forward_impl: 0 (simt) or 1 (tcgen05)");
+      c->fwd_impl = (int)value;
+    } else {
+      fail(HGNN_ERR_CONFIG, "unknown option '" + k + "'");
+    }
   });
 }
 

@@ -1,0 +1,274 @@
+// Tensor-core processor-MLP forward (sm_100a, tcgen05 kind::tf32).
+//
+// Same math as mlp_forward_kernel (mlp_simt.cuh), at fp32-equivalent accuracy
+// through a 3xTF32 split: for every linear y = a W,
+//   y = a_hi W_hi + a_hi W_lo + a_lo W_hi        (a_lo W_lo ~ 2^-22 dropped)
+// issued as two MMAs per K-step: a_hi x [W_hi | W_lo] (N = 2H) and
+// a_lo x W_hi (N = H) accumulating onto the W_lo half, so D[:, :H] + D[:, H:]
+// is the product.
+//
+// Data placement (per CTA, persistent, one CTA per SM):
+//   TMEM  2 tile slots x [A_hi (H cols) | A_lo (H cols) | D (2H cols)], 128 lanes
+//         = 512 columns at H = 64. Lane = row of the 128-row tile.
+//   SMEM  ring of weight chunks: each chunk = K = H rows of one linear as the
+//         B operand [W_hi | W_lo]^T (2H x H, K-major, SWIZZLE_NONE core
+//         matrices), laid out on the host so one cp.async.bulk moves it.
+// Warp roles: warps 0-3 epilogue of slot 0, warps 4-7 of slot 1 (thread =
+// TMEM lane = row: bias, LN0, ELU, residual, hi/lo split, all row-local),
+// warp 8 lane 0 issues MMAs, warp 9 lane 0 streams weight chunks.
+// The two slots ping-pong: the MMA of one tile runs while the other tile's
+// epilogue works, the canonical Blackwell MMA / epilogue overlap.
+#pragma once
+
+#include "mlp_simt.cuh"
+#include "tc_ptx.cuh"
+
+namespace hgnn_b200 {
+
+template <int H>
+struct TcCfg {
+  static constexpr int NB = 2 * H;                      // N of the wide MMA
+  static constexpr int CHUNK_FLOATS = NB * H;           // one K = H chunk of [W_hi | W_lo]
+  static constexpr int CHUNK_BYTES = CHUNK_FLOATS * 4;  // 32 KB at H = 64
+  static constexpr uint32_t LBO = (NB / 8) * 128;       // K-adjacent core matrices
+  static constexpr uint32_t SBO = 128;                  // N-adjacent core matrices
+  static constexpr int SLOT_COLS = 4 * H;
+  static constexpr int TMEM_COLS = 2 * SLOT_COLS;       // power of two (256 or 512)
+  static constexpr int STAGES = H == 64 ? 3 : 6;
+  static constexpr int THREADS = 320;
+  static constexpr size_t SMEM = (size_t)STAGES * CHUNK_BYTES + 1024 + 256;
+};
+
+// Host helper: byte offset of B element (n, k) inside a chunk (K-major core matrices).
+__host__ __device__ inline int64_t tc_chunk_index(int n, int k, int H) {
+  const int nb = 2 * H;
+  return (int64_t)(k / 4) * (nb / 8) * 32 + (n / 8) * 32 + (n % 8) * 4 + (k % 4);
+}
+
+struct TcFwdArgs {
+  int64_t n_rows;
+  const int32_t* src;
+  const int32_t* dst;
+  const float* x;
+  const float* e_in;
+  const float* a;
+  float* out;
+  const float* chunks;  // (nseg + k + 1) chunks in MMA order
+  const float* params;  // fp32 for_each layout (biases)
+  int k;
+};
+
+template <int H>
+__device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const float (&v)[H]) {
+#pragma unroll
+  for (int c = 0; c < H; c += 32) {
+    float hi[32], lo[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      hi[j] = ptx::tf32_rna(v[c + j]);
+      lo[j] = v[c + j] - hi[j];
+    }
+    ptx::tmem_st32(t_hi + c, hi);
+    ptx::tmem_st32(t_lo + c, lo);
+  }
+}
+
+// y[j] = D[:, j] + D[:, H + j] + b[j]
+template <int H>
+__device__ __forceinline__ void tc_load_d(uint32_t t_d, const float* __restrict__ b, float (&y)[H]) {
+#pragma unroll
+  for (int c = 0; c < H; c += 16) {
+    float p[16], q[16];
+    ptx::tmem_ld16(t_d + c, p);
+    ptx::tmem_ld16(t_d + H + c, q);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) y[c + j] = p[j] + q[j] + __ldg(b + c + j);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void tc_signal(uint64_t* bar) {
+  ptx::tmem_wait_st();
+  ptx::tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar);
+}
+
+template <int H, int MODE>
+__global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(TcFwdArgs a) {
+  using Cfg = TcCfg<H>;
+  constexpr int nseg = MODE == kEdgeInput ? 3 : 2;
+  constexpr int in_dim = nseg * H;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* wring = reinterpret_cast<float*>(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)Cfg::STAGES * Cfg::CHUNK_BYTES);
+  uint64_t* w_full = bars;                       // [STAGES]
+  uint64_t* w_empty = bars + Cfg::STAGES;        // [STAGES]
+  uint64_t* a_full = bars + 2 * Cfg::STAGES;     // [2]
+  uint64_t* a_empty = a_full + 2;                // [2]
+  uint64_t* d_full = a_empty + 2;                // [2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(d_full + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int n_chunks = nseg + a.k + 1;
+  const int64_t n_tiles = (a.n_rows + 127) / 128;
+  const int64_t n_pairs = (n_tiles + 1) / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      ptx::mbar_init(&w_full[s], 1);
+      ptx::mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&a_full[s], 4);
+      ptx::mbar_init(&a_empty[s], 1);
+      ptx::mbar_init(&d_full[s], 1);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 8) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_base_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_base_slot;
+
+  if (warp < 8) {
+    // ------------------------------------------------------------ epilogue
+    const int g = warp / 4;           // tile slot
+    const int wq = warp % 4;          // TMEM lane quarter
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    const uint32_t t_ahi = tmem + g * Cfg::SLOT_COLS + lane_off;
+    const uint32_t t_alo = t_ahi + H;
+    const uint32_t t_d = t_ahi + 2 * H;
+    uint32_t pe = 0, pd = 0;
+    for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+      const int64_t row = (2 * pair + g) * 128 + 32 * wq + lane;
+      const bool valid = row < a.n_rows;
+      float h[H];
+      // input projection: nseg K-chunks streamed through A
+      for (int c = 0; c < nseg; ++c) {
+        if (c > 0) {
+          ptx::mbar_wait(&a_empty[g], pe);
+          pe ^= 1;
+          ptx::tc_fence_after();
+        }
+        float v[H];
+        if (valid) {
+          const float* seg;
+          if (MODE == kEdgeInput)
+            seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * H
+                         : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
+          else
+            seg = c == 0 ? a.a + row * H : a.x + row * H;
+#pragma unroll
+          for (int j = 0; j < H / 4; ++j) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(seg) + j);
+            v[4 * j] = t.x;
+            v[4 * j + 1] = t.y;
+            v[4 * j + 2] = t.z;
+            v[4 * j + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < H; ++j) v[j] = 0.f;
+        }
+        tc_store_a<H>(t_ahi, t_alo, v);
+        tc_signal<H>(&a_full[g]);
+      }
+      ptx::mbar_wait(&d_full[g], pd);
+      pd ^= 1;
+      ptx::tc_fence_after();
+      tc_load_d<H>(t_d, a.params + mlp_b_offset(0, in_dim, H), h);
+      // residual blocks
+      for (int l = 1; l <= a.k; ++l) {
+        tc_store_a<H>(t_ahi, t_alo, h);
+        tc_signal<H>(&a_full[g]);
+        ptx::mbar_wait(&d_full[g], pd);
+        pd ^= 1;
+        ptx::tc_fence_after();
+        float u[H];
+        tc_load_d<H>(t_d, a.params + mlp_b_offset(l, in_dim, H), u);
+        ln0_inplace<H>(u);
+#pragma unroll
+        for (int j = 0; j < H; ++j) h[j] += elu1(u[j]);
+      }
+      // output projection
+      tc_store_a<H>(t_ahi, t_alo, h);
+      tc_signal<H>(&a_full[g]);
+      ptx::mbar_wait(&d_full[g], pd);
+      pd ^= 1;
+      ptx::tc_fence_after();
+      tc_load_d<H>(t_d, a.params + mlp_b_offset(a.k + 1, in_dim, H), h);
+      if (valid) {
+        float4* o = reinterpret_cast<float4*>(a.out + row * H);
+#pragma unroll
+        for (int j = 0; j < H / 4; ++j) o[j] = make_float4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+      }
+    }
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_wide = ptx::idesc_tf32(128, 2 * H);
+      constexpr uint32_t id_half = ptx::idesc_tf32(128, H);
+      int ws = 0;
+      uint32_t wph = 0, pa[2] = {0, 0};
+      for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        for (int j = 0; j < n_chunks; ++j) {
+          const int l = j < nseg ? 0 : j - nseg + 1;
+          const int c = j < nseg ? j : 0;
+          const bool last_chunk = (l > 0) || (c == nseg - 1);
+          ptx::mbar_wait(&w_full[ws], wph);
+          ptx::tc_fence_after();
+          const uint32_t bbase = ptx::smem_u32(wring + (size_t)ws * Cfg::CHUNK_FLOATS);
+          for (int s = 0; s < 2; ++s) {
+            ptx::mbar_wait(&a_full[s], pa[s]);
+            pa[s] ^= 1;
+            ptx::tc_fence_after();
+            const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+#pragma unroll
+            for (int ks = 0; ks < H / 8; ++ks) {
+              const uint64_t bd = ptx::smem_desc(bbase + ks * 2 * Cfg::LBO, Cfg::LBO, Cfg::SBO);
+              ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, bd, id_wide, (c > 0 || ks > 0) ? 1u : 0u);
+              ptx::mma_tf32_ts(slot + 3 * H, slot + H + 8 * ks, bd, id_half, 1u);
+            }
+            ptx::mma_commit(last_chunk ? &d_full[s] : &a_empty[s]);
+          }
+          ptx::mma_commit(&w_empty[ws]);
+          if (++ws == Cfg::STAGES) {
+            ws = 0;
+            wph ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ weight loader
+    if (lane == 0) {
+      int ws = 0;
+      uint32_t wph = 0;
+      for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        for (int j = 0; j < n_chunks; ++j) {
+          ptx::mbar_wait(&w_empty[ws], wph ^ 1);
+          ptx::mbar_arrive_expect_tx(&w_full[ws], Cfg::CHUNK_BYTES);
+          ptx::bulk_g2s(wring + (size_t)ws * Cfg::CHUNK_FLOATS, a.chunks + (size_t)j * Cfg::CHUNK_FLOATS,
+                        Cfg::CHUNK_BYTES, &w_full[ws]);
+          if (++ws == Cfg::STAGES) {
+            ws = 0;
+            wph ^= 1;
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
+  }
+}
+
+}  // namespace hgnn_b200

@@ -126,6 +126,9 @@ class Engine:
         N.check(N.LIB.hgnn_get_grads(self._h, out.ctypes.data_as(N.f64p)))
         return out
 
+    def set_option(self, key: str, value: int) -> None:
+        N.check(N.LIB.hgnn_set_option(self._h, key.encode(), int(value)))
+
     # ---- instrumentation ---------------------------------------------------
     def kernel_timing(self, enable: bool) -> None:
         N.check(N.LIB.hgnn_kernel_timing(self._h, int(enable)))

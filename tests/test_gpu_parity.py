@@ -151,3 +151,25 @@ def test_backward_before_forward_is_uninitialized(gpus):
     with pytest.raises(UninitializedError):
         eng.nmp_backward(np.zeros((g.rows, 8)))
     eng.close()
+
+
+@pytest.mark.parametrize("H,k", [(32, 5), (64, 5), (64, 0), (32, 2)])
+def test_tensor_core_forward_matches_simt_and_oracle(engine, H, k):
+    """tcgen05 3xTF32 MLP forward vs the SIMT fp32 kernels vs the fp64 oracle."""
+    M = 2
+    cfg = GnnConfig("tc", H, M, k, mode="na2a")
+    g = build_rank_graph(3, 3, 1, 0, "verify")
+    mp = mp_params(cfg, init_params(cfg, 11))
+    x0, e0, dx, de = random_inputs(g, H, 5)
+    outs = {}
+    for impl in (0, 1):
+        engine.upload_graph(g)
+        engine.configure(cfg)
+        engine.upload_params(mp)
+        engine.set_option("mlp_forward_impl", impl)
+        outs[impl] = engine.nmp_forward(x0, e0, want_e=True)
+    engine.set_option("mlp_forward_impl", 1)
+    ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
+    for impl in (0, 1):
+        assert rel(outs[impl][0], ref["x_out"][0][M - 1]) < FWD_TOL, impl
+        assert rel(outs[impl][1], ref["e_out"][0][M - 1]) < FWD_TOL, impl
