@@ -163,8 +163,16 @@ int hgnn_get_grads(hgnn_ctx* ctx, double* mp_grads);
 
 /* ---- options --------------------------------------------------------------- */
 /* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
- *                     0 = SIMT fp32 kernels. */
+ *                     0 = SIMT fp32 kernels.
+ * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
+ *                      0 = SIMT fp32 kernels. */
 int hgnn_set_option(hgnn_ctx* ctx, const char* key, int64_t value);
+
+/* ---- hardware self-test ----------------------------------------------------- */
+/* One 128 x 128 x 32 tcgen05 kind::tf32 MMA on caller data (A 128x32, B 32x128,
+ * row-major fp32; D 128x128). mode 0: A in TMEM + B K-major (forward / dX path),
+ * 1: A and B MN-major in shared memory (dW path), 2: both K-major in shared memory. */
+int hgnn_selftest_mma(int mode, const float* A, const float* B, float* D);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* When enabled, every launch of the listed kernel classes is bracketed by CUDA

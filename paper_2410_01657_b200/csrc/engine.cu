@@ -21,6 +21,7 @@
 #include "graph_kernels.cuh"
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
+#include "mlp_tc_bwd.cuh"
 
 using namespace hgnn_b200;
 
@@ -101,6 +102,10 @@ struct hgnn_ctx {
   std::vector<int64_t> chunk_off;       // per (layer, edge/node)
   DevBuf<double> grads;
   int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
+  int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
+  DevBuf<float> bchunks;                // backward chunk sequence per MLP
+  std::vector<int64_t> bchunk_off;
+  DevBuf<float> tc_scratch;
 
   // activations
   std::vector<std::unique_ptr<DevBuf<float>>> xs, es, as;
@@ -266,6 +271,31 @@ void build_chunks(const float* p, int in_dim, int H, int K, std::vector<float>& 
   }
 }
 
+// Backward chunk sequence of one MLP (mlp_tc_bwd.cuh): the forward chunks of
+// the recompute (input segments, hidden linears), then W_{k+1}^T, W_k^T .. W_1^T
+// and W_0^T per input segment. A transposed chunk stores element
+// (n = input feature, k = output feature) = W[n][k].
+void build_bwd_chunks(const float* p, int in_dim, int H, int K, std::vector<float>& out) {
+  const int nseg = in_dim / H;
+  auto emit = [&](auto elem) {
+    const size_t base = out.size();
+    out.resize(base + (size_t)2 * H * H);
+    for (int kk = 0; kk < H; ++kk)
+      for (int n = 0; n < H; ++n) {
+        const float w = elem(n, kk);
+        const float hi = tf32_rna_host(w);
+        const float lo = tf32_rna_host(w - hi);
+        out[base + (size_t)tc_chunk_index(n, kk, H)] = hi;
+        out[base + (size_t)tc_chunk_index(H + n, kk, H)] = lo;
+      }
+  };
+  auto W = [&](int l) { return p + mlp_w_offset(l, in_dim, H); };
+  for (int c = 0; c < nseg; ++c) emit([&](int n, int kk) { return W(0)[(int64_t)(c * H + kk) * H + n]; });
+  for (int l = 1; l <= K; ++l) emit([&](int n, int kk) { return W(l)[(int64_t)kk * H + n]; });
+  for (int l = K + 1; l >= 1; --l) emit([&](int n, int kk) { return W(l)[(int64_t)n * H + kk]; });
+  for (int c = 0; c < nseg; ++c) emit([&](int n, int kk) { return W(0)[(int64_t)(c * H + n) * H + kk]; });
+}
+
 // --------------------------------------------------------------------------
 // buffers
 // --------------------------------------------------------------------------
@@ -300,11 +330,12 @@ void ensure_buffers(hgnn_ctx* c) {
   plan_mlp(c, false, kEdgeInput, c->ne, c->grid_edge_b, c->smem_edge_b, c->wsm_edge_b);
   plan_mlp(c, true, kNodeInput, c->nl, c->grid_node_f, c->smem_node_f, c->wsm_node_f);
   plan_mlp(c, false, kNodeInput, c->nl, c->grid_node_b, c->smem_node_b, c->wsm_node_b);
-  const int64_t max_grid = std::max(c->grid_edge_b, c->grid_node_b);
+  const int64_t max_grid = std::max<int64_t>({c->grid_edge_b, c->grid_node_b, (int64_t)c->num_sms});
   const int64_t max_par = std::max(c->n_edge_par, c->n_node_par);
   c->grad_part.alloc(max_grid * max_par);
   const int64_t n_slots = (2 * c->K + 1) * H + c->K;
   c->scratch.alloc(max_grid * n_slots * kMlpThreads);
+  if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
   c->stage_elems = std::min<int64_t>(std::max<int64_t>(c->rows, c->ne) * H, int64_t{1} << 24);
   c->stage.alloc(std::max<int64_t>(c->stage_elems, 1));
   // halo buffers
@@ -508,6 +539,33 @@ void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const f
   }
 }
 
+bool use_tc_bwd(const hgnn_ctx* c) { return c->bwd_impl == 1 && c->H == 64; }
+
+int tc_bwd_grid(const hgnn_ctx* c, int64_t n_rows) {
+  const int64_t pairs = ((n_rows + 127) / 128 + 1) / 2;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+}
+
+// Returns the grid used (rows of grad_part written).
+int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
+  const bool edge = mode == kEdgeInput;
+  TcBwdArgs args = in;
+  args.chunks = c->bchunks.p + c->bchunk_off[(size_t)(2 * m + (edge ? 0 : 1))];
+  args.params = layer_params(c, m, edge).p;
+  args.k = (int)c->K;
+  args.scratch = c->tc_scratch.p;
+  const int grid = tc_bwd_grid(c, args.n_rows);
+  auto k = edge ? mlp_tc_backward_kernel<kEdgeInput> : mlp_tc_backward_kernel<kNodeInput>;
+  static bool attr[2] = {false, false};
+  if (!attr[edge]) {
+    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
+    attr[edge] = true;
+  }
+  k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(args);
+  check_launch(c);
+  return grid;
+}
+
 void layer_forward(hgnn_ctx* c, int64_t m) {
   const int64_t H = c->H;
   float* x = c->xs[m]->p;
@@ -578,19 +636,36 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
   {  // node update backward (model.cpp:326-340)
     Timed t(c, HGNN_K_NODE_BWD);
     CUDA_OK(cudaMemsetAsync(c->d_a.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
-    CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(c->grid_node_b * c->n_node_par), c->stream));
-    MlpRowArgs args{};
-    args.n_rows = c->nl;
-    args.x = x;
-    args.a = a;
-    args.d_out = c->dx.p;
-    args.d_a_out = c->d_a.p;
-    args.d_x_out = c->dxn.p;
-    args.grad_partial = c->grad_part.p;
-    args.scratch = c->scratch.p;
-    args.n_slots = (2 * c->K + 1) * H + c->K;
-    launch_mlp(c, false, kNodeInput, args, layer_params(c, m, false));
-    if (c->nl > 0) reduce_grads(c, c->grid_node_b, c->n_node_par, c->grads.p + goff + c->n_edge_par);
+    if (use_tc_bwd(c)) {
+      const int grid = tc_bwd_grid(c, c->nl);
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(grid * c->n_node_par), c->stream));
+      TcBwdArgs args{};
+      args.n_rows = c->nl;
+      args.x = x;
+      args.a = a;
+      args.d_out = c->dx.p;
+      args.d_a_out = c->d_a.p;
+      args.d_x_out = c->dxn.p;
+      args.grad_partial = c->grad_part.p;
+      if (c->nl > 0) {
+        launch_tc_backward(c, kNodeInput, m, args);
+        reduce_grads(c, grid, c->n_node_par, c->grads.p + goff + c->n_edge_par);
+      }
+    } else {
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(c->grid_node_b * c->n_node_par), c->stream));
+      MlpRowArgs args{};
+      args.n_rows = c->nl;
+      args.x = x;
+      args.a = a;
+      args.d_out = c->dx.p;
+      args.d_a_out = c->d_a.p;
+      args.d_x_out = c->dxn.p;
+      args.grad_partial = c->grad_part.p;
+      args.scratch = c->scratch.p;
+      args.n_slots = (2 * c->K + 1) * H + c->K;
+      launch_mlp(c, false, kNodeInput, args, layer_params(c, m, false));
+      if (c->nl > 0) reduce_grads(c, c->grid_node_b, c->n_node_par, c->grads.p + goff + c->n_edge_par);
+    }
   }
   if (c->mode != HGNN_MODE_NONE) {  // sync + exchange adjoints (model.cpp:343-351)
     if (c->n_sync > 0) {
@@ -603,23 +678,44 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
   }
   {  // aggregation + edge update backward (model.cpp:353-375)
     Timed t(c, HGNN_K_EDGE_BWD);
-    CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(c->grid_edge_b * c->n_edge_par), c->stream));
-    MlpRowArgs args{};
-    args.n_rows = c->ne;
-    args.src = c->src.p;
-    args.dst = c->dst.p;
-    args.x = x;
-    args.e_in = e;
-    args.inv_deg = c->inv.p;
-    args.d_a = c->d_a.p;
-    args.de_io = c->de.p;
-    args.d_src = c->dsrc.p;
-    args.d_dst = c->ddst.p;
-    args.grad_partial = c->grad_part.p;
-    args.scratch = c->scratch.p;
-    args.n_slots = (2 * c->K + 1) * H + c->K;
-    launch_mlp(c, false, kEdgeInput, args, layer_params(c, m, true));
-    if (c->ne > 0) reduce_grads(c, c->grid_edge_b, c->n_edge_par, c->grads.p + goff);
+    if (use_tc_bwd(c)) {
+      const int grid = tc_bwd_grid(c, c->ne);
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(grid * c->n_edge_par), c->stream));
+      TcBwdArgs args{};
+      args.n_rows = c->ne;
+      args.src = c->src.p;
+      args.dst = c->dst.p;
+      args.x = x;
+      args.e_in = e;
+      args.inv_deg = c->inv.p;
+      args.d_a = c->d_a.p;
+      args.de_io = c->de.p;
+      args.d_src = c->dsrc.p;
+      args.d_dst = c->ddst.p;
+      args.grad_partial = c->grad_part.p;
+      if (c->ne > 0) {
+        launch_tc_backward(c, kEdgeInput, m, args);
+        reduce_grads(c, grid, c->n_edge_par, c->grads.p + goff);
+      }
+    } else {
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(c->grid_edge_b * c->n_edge_par), c->stream));
+      MlpRowArgs args{};
+      args.n_rows = c->ne;
+      args.src = c->src.p;
+      args.dst = c->dst.p;
+      args.x = x;
+      args.e_in = e;
+      args.inv_deg = c->inv.p;
+      args.d_a = c->d_a.p;
+      args.de_io = c->de.p;
+      args.d_src = c->dsrc.p;
+      args.d_dst = c->ddst.p;
+      args.grad_partial = c->grad_part.p;
+      args.scratch = c->scratch.p;
+      args.n_slots = (2 * c->K + 1) * H + c->K;
+      launch_mlp(c, false, kEdgeInput, args, layer_params(c, m, true));
+      if (c->ne > 0) reduce_grads(c, c->grid_edge_b, c->n_edge_par, c->grads.p + goff);
+    }
   }
   {  // input-node adjoint (model.cpp:378-386)
     Timed t(c, HGNN_K_DX);
@@ -903,6 +999,19 @@ int hgnn_params_upload(hgnn_ctx* c, const double* flat, int64_t count) {
         }
       c->chunks.upload(ch.data(), (int64_t)ch.size(), c->stream);
     }
+    if (H == 64) {
+      std::vector<float> ch;
+      c->bchunk_off.clear();
+      int64_t poff = 0;
+      for (int64_t m = 0; m < c->M; ++m)
+        for (int which = 0; which < 2; ++which) {
+          const int in_dim = (which == 0 ? 3 : 2) * H;
+          c->bchunk_off.push_back((int64_t)ch.size());
+          build_bwd_chunks(p.data() + poff, in_dim, H, K, ch);
+          poff += mlp_param_count(in_dim, H, K);
+        }
+      c->bchunks.upload(ch.data(), (int64_t)ch.size(), c->stream);
+    }
     c->grads.alloc(std::max<int64_t>(count, 1));
     CUDA_OK(cudaStreamSynchronize(c->stream));
     c->params_ready = true;
@@ -1022,6 +1131,9 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
     if (k == "mlp_forward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_forward_impl: 0 (simt) or 1 (tcgen05)");
       c->fwd_impl = (int)value;
+    } else if (k == "mlp_backward_impl") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
+      c->bwd_impl = (int)value;
     } else {
       fail(HGNN_ERR_CONFIG, "unknown option '" + k + "'");
     }

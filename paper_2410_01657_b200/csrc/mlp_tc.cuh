@@ -1,15 +1,13 @@
 // Tensor-core processor-MLP forward (sm_100a, tcgen05 kind::tf32).
 //
-// Same math as mlp_forward_kernel (mlp_simt.cuh), at fp32-equivalent accuracy
+// Same math as mlp_forward_kernel (mlp_simt.cuh), at fp32-level accuracy
 // through a 3xTF32 split: for every linear y = a W,
 //   y = a_hi W_hi + a_hi W_lo + a_lo W_hi        (a_lo W_lo ~ 2^-22 dropped)
-// issued as two MMAs per K-step: a_hi x [W_hi | W_lo] (N = 2H) and
-// a_lo x W_hi (N = H) accumulating onto the W_lo half, so D[:, :H] + D[:, H:]
-// is the product.
+// issued as three M=128, N=H MMAs per K-step into one fp32 accumulator.
 //
 // Data placement (per CTA, persistent, one CTA per SM):
-//   TMEM  2 tile slots x [A_hi (H cols) | A_lo (H cols) | D (2H cols)], 128 lanes
-//         = 512 columns at H = 64. Lane = row of the 128-row tile.
+//   TMEM  2 tile slots x [A_hi (H cols) | A_lo (H cols) | D (H cols)], 128
+//         lanes; lane = row of the 128-row tile.
 //   SMEM  ring of weight chunks: each chunk = K = H rows of one linear as the
 //         B operand [W_hi | W_lo]^T (2H x H, K-major, SWIZZLE_NONE core
 //         matrices), laid out on the host so one cp.async.bulk moves it.
@@ -17,7 +15,8 @@
 // TMEM lane = row: bias, LN0, ELU, residual, hi/lo split, all row-local),
 // warp 8 lane 0 issues MMAs, warp 9 lane 0 streams weight chunks.
 // The two slots ping-pong: the MMA of one tile runs while the other tile's
-// epilogue works, the canonical Blackwell MMA / epilogue overlap.
+// epilogue works. Input rows (x[src], x[dst], e / a*, x) are gathered one
+// segment ahead so their latency hides behind the MMA of the previous one.
 #pragma once
 
 #include "mlp_simt.cuh"
@@ -27,19 +26,20 @@ namespace hgnn_b200 {
 
 template <int H>
 struct TcCfg {
-  static constexpr int NB = 2 * H;                      // N of the wide MMA
-  static constexpr int CHUNK_FLOATS = NB * H;           // one K = H chunk of [W_hi | W_lo]
+  static constexpr int NB = 2 * H;                      // rows of a chunk: [W_hi | W_lo]^T
+  static constexpr int CHUNK_FLOATS = NB * H;           // one K = H chunk
   static constexpr int CHUNK_BYTES = CHUNK_FLOATS * 4;  // 32 KB at H = 64
   static constexpr uint32_t LBO = (NB / 8) * 128;       // K-adjacent core matrices
   static constexpr uint32_t SBO = 128;                  // N-adjacent core matrices
-  static constexpr int SLOT_COLS = 4 * H;
-  static constexpr int TMEM_COLS = 2 * SLOT_COLS;       // power of two (256 or 512)
-  static constexpr int STAGES = H == 64 ? 3 : 6;
-  static constexpr int THREADS = 320;
-  static constexpr size_t SMEM = (size_t)STAGES * CHUNK_BYTES + 1024 + 256;
+  static constexpr uint32_t LO_OFF = (H / 8) * 128;     // start of the W_lo half
+  static constexpr int SLOT_COLS = 3 * H;
+  static constexpr int TMEM_COLS = H == 64 ? 512 : 256;  // power of two >= 2 slots
+  static constexpr int STAGES = H == 64 ? 4 : 8;
+  static constexpr int THREADS = 384;  // 2 epilogue warpgroups + 1 control warpgroup
+  static constexpr size_t SMEM = (size_t)STAGES * CHUNK_BYTES + 1024 + 256 + 18 * H * 4;  // + biases (k <= 16)
 };
 
-// Host helper: byte offset of B element (n, k) inside a chunk (K-major core matrices).
+// Index (in floats) of B element (n, k) inside a chunk (K-major core matrices).
 __host__ __device__ inline int64_t tc_chunk_index(int n, int k, int H) {
   const int nb = 2 * H;
   return (int64_t)(k / 4) * (nb / 8) * 32 + (n / 8) * 32 + (n % 8) * 4 + (k % 4);
@@ -58,6 +58,38 @@ struct TcFwdArgs {
   int k;
 };
 
+__device__ __forceinline__ float elu_fast(float z) { return z > 0.f ? z : __expf(z) - 1.0f; }
+
+// Sum of H values with 8 independent partial sums (short dependency chains).
+template <int H>
+__device__ __forceinline__ float tree_sum(const float (&v)[H]) {
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = v[i];
+#pragma unroll
+  for (int j = 8; j < H; ++j) p[j % 8] += v[j];
+  return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+}
+
+// Parameter-free LayerNorm (kernels.cpp:81-94) with tree reductions; returns inv_std.
+template <int H>
+__device__ __forceinline__ float ln0_tree(float (&v)[H]) {
+  const float mean = tree_sum<H>(v) * (1.0f / H);
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = 0.f;
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    const float d = v[j] - mean;
+    p[j % 8] = fmaf(d, d, p[j % 8]);
+  }
+  const float var = (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) * (1.0f / H);
+  const float inv_std = 1.0f / sqrtf(var + 1e-12f);
+#pragma unroll
+  for (int j = 0; j < H; ++j) v[j] = (v[j] - mean) * inv_std;
+  return inv_std;
+}
+
 template <int H>
 __device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const float (&v)[H]) {
 #pragma unroll
@@ -73,26 +105,47 @@ __device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const f
   }
 }
 
-// y[j] = D[:, j] + D[:, H + j] + b[j]
+// y[j] = D[:, j] + b[j]
 template <int H>
 __device__ __forceinline__ void tc_load_d(uint32_t t_d, const float* __restrict__ b, float (&y)[H]) {
 #pragma unroll
-  for (int c = 0; c < H; c += 16) {
-    float p[16], q[16];
-    ptx::tmem_ld16(t_d + c, p);
-    ptx::tmem_ld16(t_d + H + c, q);
+  for (int c = 0; c < H; c += 32) {
+    float p[32];
+    ptx::tmem_ld32(t_d + c, p);
     ptx::tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) y[c + j] = p[j] + q[j] + __ldg(b + c + j);
+    for (int j = 0; j < 32; ++j) y[c + j] = p[j] + b[c + j];
   }
 }
 
-template <int H>
 __device__ __forceinline__ void tc_signal(uint64_t* bar) {
   ptx::tmem_wait_st();
   ptx::tc_fence_before();
   __syncwarp();
   if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar);
+}
+
+template <int H, int MODE>
+__device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool valid, int c, float (&v)[H]) {
+  if (valid) {
+    const float* seg;
+    if (MODE == kEdgeInput)
+      seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * H
+                   : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
+    else
+      seg = c == 0 ? a.a + row * H : a.x + row * H;
+#pragma unroll
+    for (int j = 0; j < H / 4; ++j) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(seg) + j);
+      v[4 * j] = t.x;
+      v[4 * j + 1] = t.y;
+      v[4 * j + 2] = t.z;
+      v[4 * j + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < H; ++j) v[j] = 0.f;
+  }
 }
 
 template <int H, int MODE>
@@ -104,12 +157,13 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* wring = reinterpret_cast<float*>(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)Cfg::STAGES * Cfg::CHUNK_BYTES);
-  uint64_t* w_full = bars;                       // [STAGES]
-  uint64_t* w_empty = bars + Cfg::STAGES;        // [STAGES]
-  uint64_t* a_full = bars + 2 * Cfg::STAGES;     // [2]
-  uint64_t* a_empty = a_full + 2;                // [2]
-  uint64_t* d_full = a_empty + 2;                // [2]
+  uint64_t* w_full = bars;                    // [STAGES]
+  uint64_t* w_empty = bars + Cfg::STAGES;     // [STAGES]
+  uint64_t* a_full = bars + 2 * Cfg::STAGES;  // [2]
+  uint64_t* a_empty = a_full + 2;             // [2]
+  uint64_t* d_full = a_empty + 2;             // [2]
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(d_full + 2);
+  float* sbias = reinterpret_cast<float*>(smem + (size_t)Cfg::STAGES * Cfg::CHUNK_BYTES + 256);  // (k+2) x H
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -129,90 +183,96 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     }
     ptx::fence_mbarrier_init();
   }
+  for (int i = threadIdx.x; i < (a.k + 2) * H; i += blockDim.x)
+    sbias[i] = __ldg(a.params + mlp_b_offset(i / H, in_dim, H) + (i % H));
   if (warp == 8) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_base_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_base_slot;
 
+  if (warp < 8) ptx::regs_inc<224>();
+  else ptx::regs_dec<56>();
+
   if (warp < 8) {
     // ------------------------------------------------------------ epilogue
-    const int g = warp / 4;           // tile slot
-    const int wq = warp % 4;          // TMEM lane quarter
+    const int g = warp / 4;   // tile slot
+    const int wq = warp % 4;  // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     const uint32_t t_ahi = tmem + g * Cfg::SLOT_COLS + lane_off;
     const uint32_t t_alo = t_ahi + H;
     const uint32_t t_d = t_ahi + 2 * H;
     uint32_t pe = 0, pd = 0;
-    for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+    float v[H];
+    int64_t pair = blockIdx.x;
+    if (pair < n_pairs) {
+      const int64_t row0 = (2 * pair + g) * 128 + 32 * wq + lane;
+      tc_gather<H, MODE>(a, row0, row0 < a.n_rows, 0, v);
+    }
+    for (; pair < n_pairs; pair += gridDim.x) {
       const int64_t row = (2 * pair + g) * 128 + 32 * wq + lane;
       const bool valid = row < a.n_rows;
       float h[H];
-      // input projection: nseg K-chunks streamed through A
+      // input projection: nseg K-chunks streamed through A, next one prefetched
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
           ptx::mbar_wait(&a_empty[g], pe);
           pe ^= 1;
           ptx::tc_fence_after();
         }
-        float v[H];
-        if (valid) {
-          const float* seg;
-          if (MODE == kEdgeInput)
-            seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * H
-                         : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
-          else
-            seg = c == 0 ? a.a + row * H : a.x + row * H;
-#pragma unroll
-          for (int j = 0; j < H / 4; ++j) {
-            const float4 t = __ldg(reinterpret_cast<const float4*>(seg) + j);
-            v[4 * j] = t.x;
-            v[4 * j + 1] = t.y;
-            v[4 * j + 2] = t.z;
-            v[4 * j + 3] = t.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < H; ++j) v[j] = 0.f;
-        }
         tc_store_a<H>(t_ahi, t_alo, v);
-        tc_signal<H>(&a_full[g]);
+        tc_signal(&a_full[g]);
+        if (c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v);
       }
       ptx::mbar_wait(&d_full[g], pd);
       pd ^= 1;
       ptx::tc_fence_after();
-      tc_load_d<H>(t_d, a.params + mlp_b_offset(0, in_dim, H), h);
+      tc_load_d<H>(t_d, sbias, h);
       // residual blocks
       for (int l = 1; l <= a.k; ++l) {
         tc_store_a<H>(t_ahi, t_alo, h);
-        tc_signal<H>(&a_full[g]);
+        tc_signal(&a_full[g]);
         ptx::mbar_wait(&d_full[g], pd);
         pd ^= 1;
         ptx::tc_fence_after();
         float u[H];
-        tc_load_d<H>(t_d, a.params + mlp_b_offset(l, in_dim, H), u);
-        ln0_inplace<H>(u);
+        tc_load_d<H>(t_d, sbias + l * H, u);
+        ln0_tree<H>(u);
 #pragma unroll
-        for (int j = 0; j < H; ++j) h[j] += elu1(u[j]);
+        for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
       }
-      // output projection
+      // output projection; the next tile's first segment is gathered meanwhile
       tc_store_a<H>(t_ahi, t_alo, h);
-      tc_signal<H>(&a_full[g]);
+      tc_signal(&a_full[g]);
+      const int64_t next = pair + gridDim.x;
+      if (next < n_pairs) {
+        const int64_t nrow = (2 * next + g) * 128 + 32 * wq + lane;
+        tc_gather<H, MODE>(a, nrow, nrow < a.n_rows, 0, v);
+      }
       ptx::mbar_wait(&d_full[g], pd);
       pd ^= 1;
       ptx::tc_fence_after();
-      tc_load_d<H>(t_d, a.params + mlp_b_offset(a.k + 1, in_dim, H), h);
-      if (valid) {
+      {  // stream y = D + b straight to global, 32 columns at a time
+        const float* bo = sbias + (a.k + 1) * H;
         float4* o = reinterpret_cast<float4*>(a.out + row * H);
 #pragma unroll
-        for (int j = 0; j < H / 4; ++j) o[j] = make_float4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+        for (int c = 0; c < H; c += 32) {
+          float p[32];
+          ptx::tmem_ld32(t_d + c, p);
+          ptx::tmem_wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              o[c / 4 + j] = make_float4(p[4 * j] + bo[c + 4 * j], p[4 * j + 1] + bo[c + 4 * j + 1],
+                                         p[4 * j + 2] + bo[c + 4 * j + 2], p[4 * j + 3] + bo[c + 4 * j + 3]);
+          }
+        }
       }
     }
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t id_wide = ptx::idesc_tf32(128, 2 * H);
-      constexpr uint32_t id_half = ptx::idesc_tf32(128, H);
+      constexpr uint32_t idesc = ptx::idesc_tf32(128, H);
       int ws = 0;
       uint32_t wph = 0, pa[2] = {0, 0};
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
@@ -230,9 +290,12 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
             const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
 #pragma unroll
             for (int ks = 0; ks < H / 8; ++ks) {
-              const uint64_t bd = ptx::smem_desc(bbase + ks * 2 * Cfg::LBO, Cfg::LBO, Cfg::SBO);
-              ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, bd, id_wide, (c > 0 || ks > 0) ? 1u : 0u);
-              ptx::mma_tf32_ts(slot + 3 * H, slot + H + 8 * ks, bd, id_half, 1u);
+              const uint32_t kb = bbase + ks * 2 * Cfg::LBO;
+              const uint64_t b_hi = ptx::smem_desc(kb, Cfg::LBO, Cfg::SBO);
+              const uint64_t b_lo = ptx::smem_desc(kb + Cfg::LO_OFF, Cfg::LBO, Cfg::SBO);
+              ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+              ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
+              ptx::mma_tf32_ts(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
             }
             ptx::mma_commit(last_chunk ? &d_full[s] : &a_empty[s]);
           }
@@ -245,8 +308,8 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       }
     }
   } else {
-    // ------------------------------------------------------------ weight loader
-    if (lane == 0) {
+    // ------------------------------------------------------------ weight loader (warp 9; 10-11 idle)
+    if (warp == 9 && lane == 0) {
       int ws = 0;
       uint32_t wph = 0;
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {

@@ -1,0 +1,673 @@
+// Tensor-core processor-MLP backward (sm_100a, tcgen05 kind::tf32, H = 64).
+//
+// Same math as mlp_backward_kernel (mlp_simt.cuh) / mlp_backward_rows
+// (nn.cpp:204-285): recompute the forward pass of a 128-row tile, then walk the
+// linears in reverse computing the input adjoints (dX = d W^T) and the weight
+// gradients (dW += h^T d), all products as 3xTF32 on the tensor cores.
+//
+// Per CTA (persistent, one per SM), two 128-row tile slots ping-pong as in
+// the forward kernel. TMEM (512 columns):
+//   slot s: [A_hi 64 | A_lo 64 | D 64]  (s = 0, 1)      cols [192 s, 192 s + 192)
+//   dW accumulator 128 x 128                             cols [384, 512)
+// The dW product is one stacked MMA per K-step:
+//   [h_hi^T ; h_lo^T] (128 x 8) x [d_hi | d_lo] (8 x 128)
+// whose quadrants hh + hl + lh are the 3xTF32 gradient (ll is dropped). Both
+// operands are staged per warp (32 rows) in shared memory in MN-major core-
+// matrix order, through a ring of NSTAGE buffers consumed by the MMA issuer
+// in a fixed warp order (deterministic accumulation). A flush warpgroup drains
+// the accumulator after every linear into a per-CTA fp32 partial (one owning
+// thread per element: deterministic), together with the bias gradients
+// (fixed-order per-warp column sums).
+// Forward-recompute intermediates the reverse pass needs (normed t_j and
+// inv_std_j of every residual block) go to a per-CTA global scratch; the
+// residual stream is rebuilt backwards by h_{j-1} = h_j - ELU(t_j).
+// Warp roles: 0-7 epilogue (slot = warp / 4), 8 MMA issuer, 9 weight loader,
+// 10-11 idle, 12-15 dW flush.
+#pragma once
+
+#include "mlp_tc.cuh"
+
+namespace hgnn_b200 {
+
+struct TcBwdCfg {
+  static constexpr int H = 64;
+  static constexpr int CHUNK_FLOATS = 2 * H * H;
+  static constexpr int CHUNK_BYTES = CHUNK_FLOATS * 4;  // 32 KB
+  static constexpr uint32_t LBO = (2 * H / 8) * 128;   // K-major weight chunks
+  static constexpr uint32_t SBO = 128;
+  static constexpr uint32_t LO_OFF = (H / 8) * 128;
+  static constexpr int WSTAGES = 2;
+  static constexpr int NSTAGE = 4;                     // dW staging buffers
+  static constexpr int STAGE_BYTES = 32 * 1024;        // A (16 KB) + B (16 KB), 32 rows
+  // MN-major SWIZZLE_128B_BASE32B staging: atoms of 4 K-rows x 128 B of MN,
+  // 32-byte granule g of atom row r stored at granule g ^ r.
+  static constexpr uint32_t ST_LBO = 512;              // MN-atom stride (32 tf32 of MN)
+  static constexpr uint32_t ST_SBO = 2048;             // K-atom stride (4 rows): 128 MN = 4 atoms
+  static constexpr int SLOT_COLS = 3 * H;
+  static constexpr int DW_COL = 2 * SLOT_COLS;         // 384
+  static constexpr int THREADS = 512;
+  static constexpr size_t OFF_STAGE = (size_t)WSTAGES * CHUNK_BYTES;
+  static constexpr size_t OFF_BARS = OFF_STAGE + (size_t)NSTAGE * STAGE_BYTES;
+  static constexpr size_t OFF_DBP = OFF_BARS + 256;               // db partials [3][8][64]
+  static constexpr size_t OFF_XCH = OFF_DBP + 3 * 8 * 64 * 4;     // flush exchange [64][33]
+  static constexpr size_t OFF_BIAS = OFF_XCH + 64 * 33 * 4;       // biases (k+2) x 64
+  static constexpr size_t SMEM = OFF_BIAS + 18 * 64 * 4 + 1024;
+};
+
+struct TcBwdArgs {
+  int64_t n_rows;
+  const int32_t* src;
+  const int32_t* dst;
+  const float* x;
+  const float* e_in;
+  const float* a;
+  // output adjoint
+  const float* d_out;    // node mode: dx rows
+  const float* inv_deg;  // edge mode
+  const float* d_a;      // edge mode
+  float* de_io;          // edge mode: de in, de_next out (in place)
+  float* d_src;          // edge mode outputs
+  float* d_dst;
+  float* d_a_out;        // node mode outputs
+  float* d_x_out;
+  const float* chunks;   // 2 nseg + 2k + 1 chunks in MMA order
+  const float* params;   // fp32 for_each layout (biases)
+  float* grad_partial;   // [gridDim.x][n_par]
+  float* scratch;        // [gridDim.x][2][k][16][128] float4 + [gridDim.x][2][k][128] inv_std
+  int k;
+};
+
+template <int MODE>
+__device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64]) {
+  TcFwdArgs f{};
+  f.src = a.src;
+  f.dst = a.dst;
+  f.x = a.x;
+  f.e_in = a.e_in;
+  f.a = a.a;
+  tc_gather<64, MODE>(f, row, valid, c, v);
+}
+
+template <int H>
+__device__ __forceinline__ void tc_load_raw(uint32_t t_d, float (&y)[H]) {
+#pragma unroll
+  for (int c = 0; c < H; c += 32) {
+    float p[32];
+    ptx::tmem_ld32(t_d + c, p);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) y[c + j] = p[j];
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void tc_store_raw(uint32_t t_d, const float (&y)[H]) {
+#pragma unroll
+  for (int c = 0; c < H; c += 32) {
+    float p[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) p[j] = y[c + j];
+    ptx::tmem_st32(t_d + c, p);
+  }
+}
+
+// Producer side of the staging ring: use m = gi / NSTAGE of buffer gi % NSTAGE
+// waits until use m-1 was consumed. Completions of even / odd uses land on two
+// barrier sets, so the parity wait cannot alias even if use m-2 is still queued.
+__device__ __forceinline__ void stage_acquire(uint64_t* st_empty, int64_t gi) {
+  const int64_t m = gi / TcBwdCfg::NSTAGE;
+  if (m == 0) return;
+  const int buf = (int)(gi % TcBwdCfg::NSTAGE);
+  const int64_t prev = m - 1;
+  ptx::mbar_wait(&st_empty[(prev & 1) * TcBwdCfg::NSTAGE + buf], (uint32_t)((prev >> 1) & 1));
+}
+
+// Byte offset of the 16-byte group (mn = 4 mn4 .. 4 mn4 + 3, row) inside a
+// 16 KB MN-major SWIZZLE_128B_BASE32B staging operand (128 MN x 32 rows).
+// (MN-major tf32 operands must use this swizzle; SWIZZLE_NONE reads zeros.)
+__device__ __forceinline__ uint32_t st_off(int mn4, int row) {
+  const int mn = 4 * mn4, a = mn / 32, g = (mn % 32) / 8, h = (mn % 8) / 4, r = row % 4;
+  return (uint32_t)(row / 4) * TcBwdCfg::ST_SBO + (uint32_t)a * TcBwdCfg::ST_LBO + (uint32_t)r * 128 +
+         (uint32_t)((g ^ r) * 32) + (uint32_t)h * 16;
+}
+
+// Writes [v_hi | v_lo] (128 MN entries) of this lane's row into a staging operand.
+__device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&v)[64]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    float4 hi, lo;
+    hi.x = ptx::tf32_rna(v[4 * q]);
+    hi.y = ptx::tf32_rna(v[4 * q + 1]);
+    hi.z = ptx::tf32_rna(v[4 * q + 2]);
+    hi.w = ptx::tf32_rna(v[4 * q + 3]);
+    lo.x = v[4 * q] - hi.x;
+    lo.y = v[4 * q + 1] - hi.y;
+    lo.z = v[4 * q + 2] - hi.z;
+    lo.w = v[4 * q + 3] - hi.w;
+    *reinterpret_cast<float4*>(base + st_off(q, row)) = hi;
+    *reinterpret_cast<float4*>(base + st_off(16 + q, row)) = lo;
+  }
+}
+
+// Column sums of a warp's 32 x 64 tile (one row per lane), transpose-reduce:
+// lane L ends with the sums of columns 2L and 2L+1, fixed order.
+__device__ __forceinline__ float2 warp_colsum64(const float (&v)[64]) {
+  const int lane = threadIdx.x & 31;
+  float a[32];
+  // step 1 (xor 16): keep half [0,32) or [32,64)
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float send = up ? v[j] : v[32 + j];
+      const float keep = up ? v[32 + j] : v[j];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  float b[16];
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float send = up ? a[j] : a[16 + j];
+      const float keep = up ? a[16 + j] : a[j];
+      b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  float c[8];
+  {
+    const bool up = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float send = up ? b[j] : b[8 + j];
+      const float keep = up ? b[8 + j] : b[j];
+      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  float d[4];
+  {
+    const bool up = lane & 2;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float send = up ? c[j] : c[4 + j];
+      const float keep = up ? c[4 + j] : c[j];
+      d[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+  }
+  float e[2];
+  {
+    const bool up = lane & 1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float send = up ? d[j] : d[2 + j];
+      const float keep = up ? d[2 + j] : d[j];
+      e[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+  }
+  // lane bits (16,8,4,2,1) selected halves 32,16,8,4,2: column base = 32*b4 + 16*b3 + 8*b2 + 4*b1 + 2*b0
+  return make_float2(e[0], e[1]);
+}
+
+__device__ __forceinline__ int colsum_base(int lane) {
+  return 32 * ((lane >> 4) & 1) + 16 * ((lane >> 3) & 1) + 8 * ((lane >> 2) & 1) + 4 * ((lane >> 1) & 1) +
+         2 * (lane & 1);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(TcBwdArgs a) {
+  using Cfg = TcBwdCfg;
+  constexpr int H = Cfg::H;
+  constexpr int nseg = MODE == kEdgeInput ? 3 : 2;
+  constexpr int in_dim = nseg * H;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* wring = reinterpret_cast<float*>(smem);
+  uint8_t* stage = smem + Cfg::OFF_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BARS);
+  uint64_t* w_full = bars;                        // [WSTAGES]
+  uint64_t* w_empty = w_full + Cfg::WSTAGES;      // [WSTAGES]
+  uint64_t* a_full = w_empty + Cfg::WSTAGES;      // [2]
+  uint64_t* a_empty = a_full + 2;                 // [2]
+  uint64_t* d_full = a_empty + 2;                 // [2]
+  uint64_t* st_full = d_full + 2;                 // [NSTAGE]
+  uint64_t* st_empty = st_full + Cfg::NSTAGE;     // [2][NSTAGE]: split by use parity so a producer
+                                                  // running a whole job ahead cannot alias a phase
+  uint64_t* dw_full = st_empty + 2 * Cfg::NSTAGE; // [1]
+  uint64_t* dw_empty = dw_full + 1;               // [1]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(dw_empty + 1);
+  float* dbp = reinterpret_cast<float*>(smem + Cfg::OFF_DBP);
+  float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
+  float* sbias = reinterpret_cast<float*>(smem + Cfg::OFF_BIAS);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int K = a.k;
+  const int n_w = 2 * nseg + 2 * K + 1;     // weight chunks per pair
+  const int n_dw = K + 1 + nseg;            // dW jobs per pair
+  const int64_t n_tiles = (a.n_rows + 127) / 128;
+  const int64_t n_pairs = (n_tiles + 1) / 2;
+  const int64_t n_par = mlp_param_count(in_dim, H, K);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::WSTAGES; ++s) {
+      ptx::mbar_init(&w_full[s], 1);
+      ptx::mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&a_full[s], 4);
+      ptx::mbar_init(&a_empty[s], 1);
+      ptx::mbar_init(&d_full[s], 1);
+    }
+    for (int s = 0; s < Cfg::NSTAGE; ++s) {
+      ptx::mbar_init(&st_full[s], 1);
+      ptx::mbar_init(&st_empty[s], 1);
+      ptx::mbar_init(&st_empty[Cfg::NSTAGE + s], 1);
+    }
+    ptx::mbar_init(dw_full, 1);
+    ptx::mbar_init(dw_empty, 4);
+    ptx::fence_mbarrier_init();
+  }
+  for (int i = threadIdx.x; i < (K + 2) * H; i += blockDim.x)
+    sbias[i] = __ldg(a.params + mlp_b_offset(i / H, in_dim, H) + (i % H));
+  if (warp == 8) ptx::tmem_alloc<512>(tmem_base_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_base_slot;
+
+  if (warp < 8) {
+    // ================================================================ epilogue
+    const int g = warp / 4;
+    const int wq = warp % 4;
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    const uint32_t t_ahi = tmem + g * Cfg::SLOT_COLS + lane_off;
+    const uint32_t t_alo = t_ahi + H;
+    const uint32_t t_d = t_ahi + 2 * H;
+    float4* scr = reinterpret_cast<float4*>(a.scratch) + ((int64_t)blockIdx.x * 2 + g) * K * 16 * 128;
+    float* scr_inv = a.scratch + (int64_t)gridDim.x * 2 * K * 16 * 128 * 4 + ((int64_t)blockIdx.x * 2 + g) * K * 128;
+    const int trow = 32 * wq + lane;  // row inside the tile
+    uint32_t pe = 0, pd = 0;
+    int64_t job = 0;                  // global dW job counter (all pairs)
+    for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+      const int64_t row = (2 * pair + g) * 128 + trow;
+      const bool valid = row < a.n_rows;
+      float h[H];
+      // ---------------------------------------------- forward recompute
+      {
+        float v[H];
+        for (int c = 0; c < nseg; ++c) {
+          if (c > 0) {
+            ptx::mbar_wait(&a_empty[g], pe);
+            pe ^= 1;
+            ptx::tc_fence_after();
+          }
+          bwd_gather<MODE>(a, row, valid, c, v);
+          tc_store_a<H>(t_ahi, t_alo, v);
+          tc_signal(&a_full[g]);
+        }
+      }
+      ptx::mbar_wait(&d_full[g], pd);
+      pd ^= 1;
+      ptx::tc_fence_after();
+      tc_load_d<H>(t_d, sbias, h);
+      for (int l = 1; l <= K; ++l) {
+        tc_store_a<H>(t_ahi, t_alo, h);
+        tc_signal(&a_full[g]);
+        ptx::mbar_wait(&d_full[g], pd);
+        pd ^= 1;
+        ptx::tc_fence_after();
+        float u[H];
+        tc_load_d<H>(t_d, sbias + l * H, u);
+        const float inv_std = ln0_tree<H>(u);
+        float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) st[q * 128] = make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+        scr_inv[(l - 1) * 128 + trow] = inv_std;
+#pragma unroll
+        for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
+      }
+      // ---------------------------------------------- backward
+      float dh[H];
+      // output adjoint d_y (model.cpp:354-360 folded in for the edge MLP)
+      if (valid) {
+        if (MODE == kEdgeInput) {
+          const float s = __ldg(a.inv_deg + row);
+          const float4* da = reinterpret_cast<const float4*>(a.d_a + (int64_t)__ldg(a.dst + row) * H);
+          const float4* de = reinterpret_cast<const float4*>(a.de_io + row * H);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 x1 = __ldg(da + q), x2 = de[q];
+            dh[4 * q] = fmaf(s, x1.x, x2.x);
+            dh[4 * q + 1] = fmaf(s, x1.y, x2.y);
+            dh[4 * q + 2] = fmaf(s, x1.z, x2.z);
+            dh[4 * q + 3] = fmaf(s, x1.w, x2.w);
+          }
+        } else {
+          const float4* dy = reinterpret_cast<const float4*>(a.d_out + row * H);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 x1 = __ldg(dy + q);
+            dh[4 * q] = x1.x;
+            dh[4 * q + 1] = x1.y;
+            dh[4 * q + 2] = x1.z;
+            dh[4 * q + 3] = x1.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < H; ++j) dh[j] = 0.f;
+      }
+      // one backward step: d (this linear's output adjoint) is in dh; hin is
+      // the linear's input (residual stream) -> stage, A <- d, dX via MMA.
+      auto publish = [&](const float (&d)[H], const float (&hin)[H], bool with_db) {
+        tc_store_a<H>(t_ahi, t_alo, d);
+        tc_signal(&a_full[g]);
+        if (with_db) {
+          const float2 cs = warp_colsum64(d);
+          float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
+          dst[0] = cs.x;
+          dst[1] = cs.y;
+        }
+        const int64_t gi = job * 8 + warp;  // staging chunk counter
+        stage_acquire(st_empty, gi);
+        const int buf = (int)(gi % Cfg::NSTAGE);
+        uint8_t* sb = stage + (size_t)buf * Cfg::STAGE_BYTES;
+        stage_row(sb, lane, hin);
+        stage_row(sb + 16384, lane, d);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&st_full[buf]);
+      };
+      // output projection: dW_out += h_k^T d_y, d_h = d_y W_out^T
+      publish(dh, h, true);
+      ++job;
+      ptx::mbar_wait(&d_full[g], pd);
+      pd ^= 1;
+      ptx::tc_fence_after();
+      tc_load_raw<H>(t_d, dh);
+      // residual blocks in reverse (nn.cpp:259-274). The residual term of
+      // d_prev = d_u W^T + d_h is folded into the MMA by pre-loading D with d_h.
+      for (int l = K; l >= 1; --l) {
+        const float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
+        const float inv_std = scr_inv[(l - 1) * 128 + trow];
+        tc_store_raw<H>(t_d, dh);
+        float p1[8], p2[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float4 t4 = st[q * 128];
+          const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * q + u;
+            const float t = tv[u];
+            const float ex = __expf(t);
+            const float elu = t > 0.f ? t : ex - 1.0f;
+            const float dd = dh[j] * (t > 0.f ? 1.0f : ex);  // elu', kernels.cpp:68-71
+            h[j] -= elu;                                     // h_{l-1}
+            dh[j] = dd;
+            p1[j % 8] += dd;
+            p2[j % 8] = fmaf(dd, t, p2[j % 8]);
+          }
+        }
+        const float g_mean = (((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]))) * (1.0f / H);
+        const float gx_mean =
+            (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float4 t4 = st[q * 128];
+          dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
+          dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
+          dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
+          dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
+        }
+        publish(dh, h, true);
+        ++job;
+        ptx::mbar_wait(&d_full[g], pd);
+        pd ^= 1;
+        ptx::tc_fence_after();
+        tc_load_raw<H>(t_d, dh);
+      }
+      // input projection (nn.cpp:277-281): per segment c, dW0[seg c] and d_in[seg c]
+      tc_store_a<H>(t_ahi, t_alo, dh);
+      tc_signal(&a_full[g]);
+      {
+        const float2 cs = warp_colsum64(dh);
+        float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
+        dst[0] = cs.x;
+        dst[1] = cs.y;
+      }
+      for (int c = 0; c < nseg; ++c) {
+        {
+          float xin[H];
+          bwd_gather<MODE>(a, row, valid, c, xin);
+          const int64_t gi = job * 8 + warp;
+          stage_acquire(st_empty, gi);
+          const int buf = (int)(gi % Cfg::NSTAGE);
+          uint8_t* sb = stage + (size_t)buf * Cfg::STAGE_BYTES;
+          stage_row(sb, lane, xin);
+          stage_row(sb + 16384, lane, dh);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&st_full[buf]);
+        }
+        ++job;
+        ptx::mbar_wait(&d_full[g], pd);
+        pd ^= 1;
+        ptx::tc_fence_after();
+        float* outp;
+        if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
+        else outp = c == 0 ? a.d_a_out : a.d_x_out;
+        float4* o = reinterpret_cast<float4*>(outp + row * H);
+#pragma unroll
+        for (int cc = 0; cc < H; cc += 32) {
+          float p[32];
+          ptx::tmem_ld32(t_d + cc, p);
+          ptx::tmem_wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[cc / 4 + j] = make_float4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+          }
+        }
+        if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays
+      }
+    }
+  } else if (warp == 8) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_tf32(128, H);
+      constexpr uint32_t idesc_dw = ptx::idesc_tf32(128, 2 * H) | (1u << 15) | (1u << 16);  // A, B MN-major
+      int ws = 0;
+      uint32_t wph = 0, pa[2] = {0, 0}, pdw = 0;
+      int64_t gi = 0;  // staging chunk counter
+      auto mma3 = [&](int s, uint32_t bbase, bool first_zero) {
+        const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+#pragma unroll
+        for (int ks = 0; ks < H / 8; ++ks) {
+          const uint32_t kb = bbase + ks * 2 * Cfg::LBO;
+          const uint64_t b_hi = ptx::smem_desc(kb, Cfg::LBO, Cfg::SBO);
+          const uint64_t b_lo = ptx::smem_desc(kb + Cfg::LO_OFF, Cfg::LBO, Cfg::SBO);
+          ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (!first_zero || ks > 0) ? 1u : 0u);
+          ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
+          ptx::mma_tf32_ts(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
+        }
+      };
+      auto next_w = [&]() -> uint32_t {
+        ptx::mbar_wait(&w_full[ws], wph);
+        ptx::tc_fence_after();
+        return ptx::smem_u32(wring + (size_t)ws * Cfg::CHUNK_FLOATS);
+      };
+      auto release_w = [&]() {
+        ptx::mma_commit(&w_empty[ws]);
+        if (++ws == Cfg::WSTAGES) {
+          ws = 0;
+          wph ^= 1;
+        }
+      };
+      auto dw_job = [&]() {
+        ptx::mbar_wait(dw_empty, pdw ^ 1);
+        ptx::tc_fence_after();
+        for (int b = 0; b < 8; ++b, ++gi) {
+          const int buf = (int)(gi % Cfg::NSTAGE);
+          const uint32_t par = (uint32_t)((gi / Cfg::NSTAGE) & 1);
+          ptx::mbar_wait(&st_full[buf], par);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(stage + (size_t)buf * Cfg::STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            constexpr uint64_t swz = (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+            const uint64_t ad = ptx::smem_desc(sa + ks * 2 * Cfg::ST_SBO, Cfg::ST_LBO, Cfg::ST_SBO) | swz;
+            const uint64_t bd = ptx::smem_desc(sa + 16384 + ks * 2 * Cfg::ST_SBO, Cfg::ST_LBO, Cfg::ST_SBO) | swz;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + Cfg::DW_COL),
+                "l"(ad), "l"(bd), "r"(idesc_dw), "r"((b > 0 || ks > 0) ? 1u : 0u)
+                : "memory");
+          }
+          ptx::mma_commit(&st_empty[((gi / Cfg::NSTAGE) & 1) * Cfg::NSTAGE + buf]);
+        }
+        ptx::mma_commit(dw_full);
+        pdw ^= 1;
+      };
+      for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        // forward recompute: input chunks then hidden blocks (no output linear)
+        for (int c = 0; c < nseg; ++c) {
+          const uint32_t bb = next_w();
+          for (int s = 0; s < 2; ++s) {
+            ptx::mbar_wait(&a_full[s], pa[s]);
+            pa[s] ^= 1;
+            ptx::tc_fence_after();
+            mma3(s, bb, c == 0);
+            ptx::mma_commit(c + 1 < nseg ? &a_empty[s] : &d_full[s]);
+          }
+          release_w();
+        }
+        for (int l = 1; l <= K; ++l) {
+          const uint32_t bb = next_w();
+          for (int s = 0; s < 2; ++s) {
+            ptx::mbar_wait(&a_full[s], pa[s]);
+            pa[s] ^= 1;
+            ptx::tc_fence_after();
+            mma3(s, bb, true);
+            ptx::mma_commit(&d_full[s]);
+          }
+          release_w();
+        }
+        // backward: output linear, hidden blocks in reverse (dX then dW each);
+        // hidden steps accumulate onto D pre-loaded with the residual d_h
+        for (int step = 0; step <= K; ++step) {
+          const uint32_t bb = next_w();
+          for (int s = 0; s < 2; ++s) {
+            ptx::mbar_wait(&a_full[s], pa[s]);
+            pa[s] ^= 1;
+            ptx::tc_fence_after();
+            mma3(s, bb, step == 0);
+            ptx::mma_commit(&d_full[s]);
+          }
+          release_w();
+          dw_job();
+        }
+        // input linear: per segment, dX then dW
+        for (int c = 0; c < nseg; ++c) {
+          const uint32_t bb = next_w();
+          for (int s = 0; s < 2; ++s) {
+            ptx::mbar_wait(&a_full[s], pa[s]);
+            pa[s] ^= 1;
+            ptx::tc_fence_after();
+            mma3(s, bb, true);
+            ptx::mma_commit(&d_full[s]);
+          }
+          release_w();
+          dw_job();
+        }
+      }
+    }
+  } else if (warp == 9 || warp == 10 || warp == 11) {
+    // ================================================================ loader
+    if (warp == 9 && lane == 0) {
+      int ws = 0;
+      uint32_t wph = 0;
+      for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        for (int j = 0; j < n_w; ++j) {
+          ptx::mbar_wait(&w_empty[ws], wph ^ 1);
+          ptx::mbar_arrive_expect_tx(&w_full[ws], Cfg::CHUNK_BYTES);
+          ptx::bulk_g2s(wring + (size_t)ws * Cfg::CHUNK_FLOATS, a.chunks + (size_t)j * Cfg::CHUNK_FLOATS,
+                        Cfg::CHUNK_BYTES, &w_full[ws]);
+          if (++ws == Cfg::WSTAGES) {
+            ws = 0;
+            wph ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ================================================================ dW flush (warps 12-15)
+    const int wq = warp % 4;
+    const int L = 32 * wq + lane;  // TMEM lane owned
+    const uint32_t t_dw = tmem + Cfg::DW_COL + ((uint32_t)(32 * wq) << 16);
+    float* gpart = a.grad_partial + (int64_t)blockIdx.x * n_par;
+    uint32_t pdw = 0;
+    int64_t job = 0;
+    for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+      for (int jj = 0; jj < n_dw; ++jj, ++job) {
+        // which linear / rows this job covers
+        int lin, rowbase;
+        bool with_db;
+        if (jj <= K) {
+          lin = K + 1 - jj;  // out (K+1), then K..1
+          rowbase = 0;
+          with_db = true;
+        } else {
+          lin = 0;
+          rowbase = (jj - K - 1) * H;
+          with_db = jj == K + 1;
+        }
+        ptx::mbar_wait(dw_full, pdw);
+        pdw ^= 1;
+        ptx::tc_fence_after();
+        float* gw = gpart + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + (L & 63)) * H;
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          float p[32];
+          ptx::tmem_ld32(t_dw + c, p);
+          ptx::tmem_wait_ld();
+          if (L < 64) {
+            float q[32];
+            ptx::tmem_ld32(t_dw + 64 + c, q);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) p[j] += q[j];  // hh + hl
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xch[(L - 64) * 33 + j] = p[j];  // lh
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (L < 64) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) gw[c + j] += p[j] + xch[L * 33 + j];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        ptx::tc_fence_before();
+        if (lane == 0) ptx::mbar_arrive(dw_empty);  // accumulator may be overwritten now
+        if (L < 64 && with_db) {
+          const float* db = dbp + (job % 3) * 8 * 64;
+          float sdb = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sdb += db[w * 64 + L];
+          gpart[mlp_b_offset(lin, in_dim, H) + L] += sdb;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace hgnn_b200

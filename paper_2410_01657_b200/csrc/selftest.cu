@@ -1,0 +1,143 @@
+// Hardware self-tests of the tcgen05 building blocks used by the MLP kernels:
+// one 128-row MMA (K = 32) in each operand configuration, on caller data.
+//   mode 0: A in TMEM (TS), B K-major in SMEM          (forward / dX path)
+//   mode 1: A, B both MN-major in SMEM (SS), N = 128   (dW path)
+//   mode 2: A, B both K-major in SMEM (SS), N = 128
+// A: 128 x 32 (row-major m, k), B: 32 x N (row-major k, n), D = A B (fp32 out).
+#include <cstring>
+#include <vector>
+
+#include "common.hpp"
+#include "tc_ptx.cuh"
+
+using namespace hgnn_b200;
+
+namespace {
+
+constexpr int TM = 128, TK = 32, TN = 128;
+
+// K-major core-matrix offset (bytes) of element (mn, k): 8 MN rows x 16 B of K
+__device__ uint32_t kmaj(int mn, int k, int n_mn) {
+  const uint32_t lbo = (uint32_t)(n_mn / 8) * 128;  // K-chunk stride
+  return (uint32_t)(k / 4) * lbo + (uint32_t)(mn / 8) * 128 + (uint32_t)(mn % 8) * 16 + (uint32_t)(k % 4) * 4;
+}
+// MN-major SWIZZLE_128B_BASE32B: atoms of 4 K-rows x 128 B of MN (32 tf32);
+// 32-byte granule g of row r stored at granule g ^ r. Atoms: MN stride lbo,
+// K stride sbo.
+__device__ uint32_t mn_sw(int mn, int k, uint32_t lbo, uint32_t sbo) {
+  const int a = mn / 32, w = mn % 32, g = w / 8, e = w % 8, r = k % 4;
+  return (uint32_t)(k / 4) * sbo + (uint32_t)a * lbo + (uint32_t)r * 128 + (uint32_t)((g ^ r) * 32) + (uint32_t)e * 4;
+}
+// MN-major core-matrix offset (bytes): 8 K rows x 16 B of MN
+__device__ uint32_t mnmaj(int mn, int k, int n_k) {
+  const uint32_t sbo = (uint32_t)(n_k / 8) * 128;  // MN-chunk stride
+  return (uint32_t)(mn / 4) * sbo + (uint32_t)(k / 8) * 128 + (uint32_t)(k % 8) * 16 + (uint32_t)(mn % 4) * 4;
+}
+
+__global__ void __launch_bounds__(128) selftest_kernel(int mode, const float* A, const float* B, float* D) {
+  __shared__ __align__(1024) uint8_t sa[TM * TK * 4];
+  __shared__ __align__(1024) uint8_t sb[TK * TN * 4];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int t = threadIdx.x;
+  const int warp = t / 32;
+  // stage operands
+  const bool sw = mode >= 6;
+  const bool a_mn = mode == 1 || mode == 3 || mode == 5 || mode == 6 || mode == 7;
+  const bool b_mn = mode == 1 || mode == 4 || mode == 5 || mode == 6 || mode == 8;
+  // swizzled MN-major: MN atoms (128 B) at lbo = 512, K atoms (4 rows) at sbo = (MN/32) * 512
+  const uint32_t sw_lbo = 512, sw_sbo_a = (TM / 32) * 512, sw_sbo_b = (TN / 32) * 512;
+  for (int i = t; i < TM * TK; i += 128) {
+    const int m = i / TK, k = i % TK;
+    const uint32_t off = (sw && a_mn) ? mn_sw(m, k, sw_lbo, sw_sbo_a) : (a_mn ? mnmaj(m, k, TK) : kmaj(m, k, TM));
+    *reinterpret_cast<float*>(sa + off) = A[i];
+  }
+  for (int i = t; i < TK * TN; i += 128) {
+    const int k = i / TN, n = i % TN;
+    const uint32_t off = (sw && b_mn) ? mn_sw(n, k, sw_lbo, sw_sbo_b) : (b_mn ? mnmaj(n, k, TK) : kmaj(n, k, TN));
+    *reinterpret_cast<float*>(sb + off) = B[i];
+  }
+  if (t == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<256>(&tslot);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+  if (mode == 0) {  // A into TMEM columns [128, 160): thread = row
+    float v[32];
+    for (int k = 0; k < 32; ++k) v[k] = A[t * TK + k];
+    ptx::tmem_st32(tmem + 128 + lane_off, v);
+    ptx::tmem_wait_st();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (t == 0) {
+    const uint32_t a_s = ptx::smem_u32(sa), b_s = ptx::smem_u32(sb);
+    for (int ks = 0; ks < TK / 8; ++ks) {
+      if (mode == 0) {
+        const uint32_t lbo = (TN / 8) * 128;  // N = 128 K-major
+        const uint64_t bd = ptx::smem_desc(b_s + ks * 2 * lbo, lbo, 128);
+        ptx::mma_tf32_ts(tmem, tmem + 128 + 8 * ks, bd, ptx::idesc_tf32(128, TN), ks > 0);
+      } else {
+        uint64_t ad, bd;
+        uint32_t idesc = ptx::idesc_tf32(128, TN);
+        const uint32_t lbo_a = (TM / 8) * 128, lbo_b = (TN / 8) * 128;
+        const uint32_t mn_lbo = mode == 5 ? (TK / 8) * 128 : 128, mn_sbo = mode == 5 ? 128 : (TK / 8) * 128;
+        ad = a_mn ? ptx::smem_desc(a_s + ks * 128, mn_lbo, mn_sbo) : ptx::smem_desc(a_s + ks * 2 * lbo_a, lbo_a, 128);
+        bd = b_mn ? ptx::smem_desc(b_s + ks * 128, mn_lbo, mn_sbo) : ptx::smem_desc(b_s + ks * 2 * lbo_b, lbo_b, 128);
+        if (sw) {
+          const uint64_t swz = (uint64_t)1 << 61;  // layout type 1 = SWIZZLE_128B_BASE32B
+          if (a_mn) ad = ptx::smem_desc(a_s + ks * 2 * sw_sbo_a, sw_lbo, sw_sbo_a) | swz;
+          if (b_mn) bd = ptx::smem_desc(b_s + ks * 2 * sw_sbo_b, sw_lbo, sw_sbo_b) | swz;
+        }
+        if (a_mn) idesc |= (1u << 15);
+        if (b_mn) idesc |= (1u << 16);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1u : 0u)
+            : "memory");
+      }
+    }
+    ptx::mma_commit(&bar);
+  }
+  ptx::mbar_wait(&bar, 0);
+  ptx::tc_fence_after();
+  for (int c = 0; c < TN; c += 32) {
+    float v[32];
+    ptx::tmem_ld32(tmem + lane_off + c, v);
+    ptx::tmem_wait_ld();
+    for (int j = 0; j < 32; ++j) D[t * TN + c + j] = v[j];
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<256>(tmem);
+  }
+}
+
+}  // namespace
+
+extern "C" int hgnn_selftest_mma(int mode, const float* A, const float* B, float* D) {
+  return guarded([&] {
+    float *dA, *dB, *dD;
+    if (cudaMalloc(&dA, TM * TK * 4) || cudaMalloc(&dB, TK * TN * 4) || cudaMalloc(&dD, TM * TN * 4))
+      fail(HGNN_ERR_CUDA, "selftest alloc");
+    cudaMemcpy(dA, A, TM * TK * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, B, TK * TN * 4, cudaMemcpyHostToDevice);
+    selftest_kernel<<<1, 128>>>(mode, dA, dB, dD);
+    const cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(D, dD, TM * TN * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dD);
+    if (e != cudaSuccess) fail(HGNN_ERR_CUDA, cudaGetErrorString(e));
+  });
+}

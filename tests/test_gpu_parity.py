@@ -173,3 +173,28 @@ def test_tensor_core_forward_matches_simt_and_oracle(engine, H, k):
     for impl in (0, 1):
         assert rel(outs[impl][0], ref["x_out"][0][M - 1]) < FWD_TOL, impl
         assert rel(outs[impl][1], ref["e_out"][0][M - 1]) < FWD_TOL, impl
+
+
+@pytest.mark.parametrize("E,p,k,M", [(3, 3, 5, 2), (3, 5, 2, 1), (2, 4, 0, 1), (4, 5, 5, 2)])
+def test_tensor_core_backward_matches_simt_and_oracle(engine, E, p, k, M):
+    """tcgen05 3xTF32 MLP backward (dX chain + stacked dW MMAs) vs SIMT vs fp64 oracle."""
+    H = 64
+    cfg = GnnConfig("tcb", H, M, k, mode="na2a")
+    g = build_rank_graph(E, p, 1, 0, "verify")
+    mp = mp_params(cfg, init_params(cfg, 21))
+    x0, e0, dx, de = random_inputs(g, H, 9)
+    res = {}
+    for impl in (0, 1):
+        engine.upload_graph(g)
+        engine.configure(cfg)
+        engine.upload_params(mp)
+        engine.set_option("mlp_backward_impl", impl)
+        engine.nmp_forward(x0, e0)
+        res[impl] = engine.nmp_backward(dx, de)
+    engine.set_option("mlp_backward_impl", 1)
+    ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
+    for impl in (0, 1):
+        dx0, de0, grads = res[impl]
+        assert rel(dx0, ref["dx_in"][0][0]) < BWD_TOL, (impl, rel(dx0, ref["dx_in"][0][0]))
+        assert rel(de0, ref["de_in"][0][0]) < BWD_TOL, (impl, rel(de0, ref["de_in"][0][0]))
+        assert grad_rel(grads, ref["grads"][0], cfg) < BWD_TOL, (impl, grad_rel(grads, ref["grads"][0], cfg))
