@@ -106,6 +106,8 @@ struct hgnn_ctx {
   DevBuf<float> bchunks;                // backward chunk sequence per MLP
   std::vector<int64_t> bchunk_off;
   DevBuf<float> tc_scratch;
+  DevBuf<unsigned long long> prof;      // optional backward-kernel wait profile
+  bool prof_on = false;
 
   // activations
   std::vector<std::unique_ptr<DevBuf<float>>> xs, es, as;
@@ -332,7 +334,7 @@ void ensure_buffers(hgnn_ctx* c) {
   plan_mlp(c, false, kNodeInput, c->nl, c->grid_node_b, c->smem_node_b, c->wsm_node_b);
   const int64_t max_grid = std::max<int64_t>({c->grid_edge_b, c->grid_node_b, (int64_t)c->num_sms});
   const int64_t max_par = std::max(c->n_edge_par, c->n_node_par);
-  c->grad_part.alloc(max_grid * max_par);
+  c->grad_part.alloc(2 * max_grid * max_par);  // tcgen05 backward keeps two partials per CTA
   const int64_t n_slots = (2 * c->K + 1) * H + c->K;
   c->scratch.alloc(max_grid * n_slots * kMlpThreads);
   if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
@@ -554,12 +556,15 @@ int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
   args.params = layer_params(c, m, edge).p;
   args.k = (int)c->K;
   args.scratch = c->tc_scratch.p;
+  args.prof = c->prof_on ? c->prof.p + (edge ? 0 : kProfCount) : nullptr;
   const int grid = tc_bwd_grid(c, args.n_rows);
-  auto k = edge ? mlp_tc_backward_kernel<kEdgeInput> : mlp_tc_backward_kernel<kNodeInput>;
-  static bool attr[2] = {false, false};
-  if (!attr[edge]) {
+  const bool prof = args.prof != nullptr;
+  auto k = edge ? (prof ? mlp_tc_backward_kernel<kEdgeInput, true> : mlp_tc_backward_kernel<kEdgeInput, false>)
+                : (prof ? mlp_tc_backward_kernel<kNodeInput, true> : mlp_tc_backward_kernel<kNodeInput, false>);
+  static bool attr[2][2] = {{false, false}, {false, false}};
+  if (!attr[edge][prof]) {
     CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
-    attr[edge] = true;
+    attr[edge][prof] = true;
   }
   k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(args);
   check_launch(c);
@@ -638,7 +643,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
     CUDA_OK(cudaMemsetAsync(c->d_a.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
     if (use_tc_bwd(c)) {
       const int grid = tc_bwd_grid(c, c->nl);
-      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(grid * c->n_node_par), c->stream));
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * grid * c->n_node_par), c->stream));
       TcBwdArgs args{};
       args.n_rows = c->nl;
       args.x = x;
@@ -649,7 +654,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.grad_partial = c->grad_part.p;
       if (c->nl > 0) {
         launch_tc_backward(c, kNodeInput, m, args);
-        reduce_grads(c, grid, c->n_node_par, c->grads.p + goff + c->n_edge_par);
+        reduce_grads(c, 2 * grid, c->n_node_par, c->grads.p + goff + c->n_edge_par);
       }
     } else {
       CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(c->grid_node_b * c->n_node_par), c->stream));
@@ -680,7 +685,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
     Timed t(c, HGNN_K_EDGE_BWD);
     if (use_tc_bwd(c)) {
       const int grid = tc_bwd_grid(c, c->ne);
-      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(grid * c->n_edge_par), c->stream));
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * grid * c->n_edge_par), c->stream));
       TcBwdArgs args{};
       args.n_rows = c->ne;
       args.src = c->src.p;
@@ -695,7 +700,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.grad_partial = c->grad_part.p;
       if (c->ne > 0) {
         launch_tc_backward(c, kEdgeInput, m, args);
-        reduce_grads(c, grid, c->n_edge_par, c->grads.p + goff);
+        reduce_grads(c, 2 * grid, c->n_edge_par, c->grads.p + goff);
       }
     } else {
       CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(c->grid_edge_b * c->n_edge_par), c->stream));
@@ -1131,6 +1136,10 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
     if (k == "mlp_forward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_forward_impl: 0 (simt) or 1 (tcgen05)");
       c->fwd_impl = (int)value;
+    } else if (k == "bwd_profile") {
+      c->prof.alloc(2 * kProfCount);
+      CUDA_OK(cudaMemsetAsync(c->prof.p, 0, sizeof(unsigned long long) * 2 * kProfCount, c->stream));
+      c->prof_on = value != 0;
     } else if (k == "mlp_backward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
       c->bwd_impl = (int)value;
@@ -1162,6 +1171,14 @@ int hgnn_kernel_time(hgnn_ctx* c, int cls, double* total_ms, int64_t* launches) 
     }
     *total_ms = t;
     *launches = (int64_t)c->ev_used[cls];
+  });
+}
+
+int hgnn_debug_profile(hgnn_ctx* c, uint64_t* out16) {
+  return guarded([&] {
+    bind(c);
+    if (!c->prof.p) fail(HGNN_ERR_UNINITIALIZED, "bwd_profile not enabled");
+    CUDA_OK(cudaMemcpy(out16, c->prof.p, sizeof(unsigned long long) * 2 * kProfCount, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -97,7 +97,7 @@ __device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const f
     float hi[32], lo[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      hi[j] = ptx::tf32_rna(v[c + j]);
+      hi[j] = ptx::tf32_trunc(v[c + j]);
       lo[j] = v[c + j] - hi[j];
     }
     ptx::tmem_st32(t_hi + c, hi);

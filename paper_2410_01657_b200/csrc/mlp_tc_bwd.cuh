@@ -12,17 +12,20 @@
 // The dW product is one stacked MMA per K-step:
 //   [h_hi^T ; h_lo^T] (128 x 8) x [d_hi | d_lo] (8 x 128)
 // whose quadrants hh + hl + lh are the 3xTF32 gradient (ll is dropped). Both
-// operands are staged per warp (32 rows) in shared memory in MN-major core-
-// matrix order, through a ring of NSTAGE buffers consumed by the MMA issuer
-// in a fixed warp order (deterministic accumulation). A flush warpgroup drains
-// the accumulator after every linear into a per-CTA fp32 partial (one owning
-// thread per element: deterministic), together with the bias gradients
-// (fixed-order per-warp column sums).
-// Forward-recompute intermediates the reverse pass needs (normed t_j and
-// inv_std_j of every residual block) go to a per-CTA global scratch; the
-// residual stream is rebuilt backwards by h_{j-1} = h_j - ELU(t_j).
-// Warp roles: 0-7 epilogue (slot = warp / 4), 8 MMA issuer, 9 weight loader,
-// 10-11 idle, 12-15 dW flush.
+// operands are staged per warp (32 rows) in shared memory as MN-major
+// SWIZZLE_128B_BASE32B tiles (the layout tf32 MN-major operands require),
+// through a ring of NSTAGE buffers consumed by the MMA issuer in a fixed warp
+// order (deterministic accumulation). The epilogue warps drain the
+// accumulator of job j before staging job j + 1 (whose ring slots are only
+// recycled by MMAs onto that accumulator): each warp owns its TMEM lane quarter and one column
+// half, adding hh + hl into a per-CTA fp32 partial and lh into a second one
+// (one owning thread per element: deterministic); bias gradients come from
+// fixed-order per-warp column sums.
+// Forward-recompute intermediates of the reverse pass (normed t_j, inv_std_j)
+// go to a per-CTA global scratch; the residual stream is rebuilt backwards as
+// h_{j-1} = h_j - ELU(t_j). The residual term of d_prev = d_u W^T + d_h is
+// folded into the MMA by pre-loading D with d_h.
+// Warp roles: 0-7 epilogue (slot = warp / 4), 8 MMA issuer, 9 weight loader, 10-11 idle.
 #pragma once
 
 #include "mlp_tc.cuh"
@@ -45,12 +48,11 @@ struct TcBwdCfg {
   static constexpr uint32_t ST_SBO = 2048;             // K-atom stride (4 rows): 128 MN = 4 atoms
   static constexpr int SLOT_COLS = 3 * H;
   static constexpr int DW_COL = 2 * SLOT_COLS;         // 384
-  static constexpr int THREADS = 512;
+  static constexpr int THREADS = 384;  // 2 epilogue warpgroups + 1 control warpgroup
   static constexpr size_t OFF_STAGE = (size_t)WSTAGES * CHUNK_BYTES;
   static constexpr size_t OFF_BARS = OFF_STAGE + (size_t)NSTAGE * STAGE_BYTES;
   static constexpr size_t OFF_DBP = OFF_BARS + 256;               // db partials [3][8][64]
-  static constexpr size_t OFF_XCH = OFF_DBP + 3 * 8 * 64 * 4;     // flush exchange [64][33]
-  static constexpr size_t OFF_BIAS = OFF_XCH + 64 * 33 * 4;       // biases (k+2) x 64
+  static constexpr size_t OFF_BIAS = OFF_DBP + 3 * 8 * 64 * 4;    // biases (k+2) x 64
   static constexpr size_t SMEM = OFF_BIAS + 18 * 64 * 4 + 1024;
 };
 
@@ -72,10 +74,15 @@ struct TcBwdArgs {
   float* d_x_out;
   const float* chunks;   // 2 nseg + 2k + 1 chunks in MMA order
   const float* params;   // fp32 for_each layout (biases)
-  float* grad_partial;   // [gridDim.x][n_par]
+  float* grad_partial;   // [gridDim.x][2][n_par]: (hh + hl, db) and lh partials
   float* scratch;        // [gridDim.x][2][k][16][128] float4 + [gridDim.x][2][k][128] inv_std
   int k;
+  unsigned long long* prof;  // optional: wait-cycle counters (see kProf*)
 };
+
+// Optional instrumentation of the MMA issuer (cycles, summed over CTAs).
+enum { kProfTotal = 0, kProfW = 1, kProfA = 2, kProfSt = 3, kProfDwE = 4, kProfFwd = 5, kProfDw = 6, kProfMma = 7,
+       kProfCount = 8 };
 
 template <int MODE>
 __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64]) {
@@ -88,26 +95,48 @@ __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool
   tc_gather<64, MODE>(f, row, valid, c, v);
 }
 
-template <int H>
-__device__ __forceinline__ void tc_load_raw(uint32_t t_d, float (&y)[H]) {
+// Scratch reload that the compiler may not merge with an earlier load of the
+// same address (keeps the 64 normed values out of registers between passes).
+__device__ __forceinline__ float4 ld_reload(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+
+// A <- [hi | lo] split of v, 16 columns at a time (low register pressure).
+__device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const float (&v)[64]) {
 #pragma unroll
-  for (int c = 0; c < H; c += 32) {
-    float p[32];
-    ptx::tmem_ld32(t_d + c, p);
-    ptx::tmem_wait_ld();
+  for (int c = 0; c < 64; c += 16) {
+    float hi[16], lo[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) y[c + j] = p[j];
+    for (int j = 0; j < 16; ++j) {
+      hi[j] = ptx::tf32_trunc(v[c + j]);
+      lo[j] = v[c + j] - hi[j];
+    }
+    ptx::tmem_st16(t_hi + c, hi);
+    ptx::tmem_st16(t_lo + c, lo);
   }
 }
 
-template <int H>
-__device__ __forceinline__ void tc_store_raw(uint32_t t_d, const float (&y)[H]) {
+// y = D (+ b), 16 columns at a time.
+__device__ __forceinline__ void bwd_load_d(uint32_t t_d, const float* b, float (&y)[64]) {
 #pragma unroll
-  for (int c = 0; c < H; c += 32) {
-    float p[32];
+  for (int c = 0; c < 64; c += 16) {
+    float p[16];
+    ptx::tmem_ld16(t_d + c, p);
+    ptx::tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) p[j] = y[c + j];
-    ptx::tmem_st32(t_d + c, p);
+    for (int j = 0; j < 16; ++j) y[c + j] = b ? p[j] + b[c + j] : p[j];
+  }
+}
+
+__device__ __forceinline__ void bwd_store_raw(uint32_t t_d, const float (&y)[64]) {
+#pragma unroll
+  for (int c = 0; c < 64; c += 16) {
+    float p[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) p[j] = y[c + j];
+    ptx::tmem_st16(t_d + c, p);
   }
 }
 
@@ -136,10 +165,10 @@ __device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     float4 hi, lo;
-    hi.x = ptx::tf32_rna(v[4 * q]);
-    hi.y = ptx::tf32_rna(v[4 * q + 1]);
-    hi.z = ptx::tf32_rna(v[4 * q + 2]);
-    hi.w = ptx::tf32_rna(v[4 * q + 3]);
+    hi.x = ptx::tf32_trunc(v[4 * q]);
+    hi.y = ptx::tf32_trunc(v[4 * q + 1]);
+    hi.z = ptx::tf32_trunc(v[4 * q + 2]);
+    hi.w = ptx::tf32_trunc(v[4 * q + 3]);
     lo.x = v[4 * q] - hi.x;
     lo.y = v[4 * q + 1] - hi.y;
     lo.z = v[4 * q + 2] - hi.z;
@@ -154,7 +183,6 @@ __device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&
 __device__ __forceinline__ float2 warp_colsum64(const float (&v)[64]) {
   const int lane = threadIdx.x & 31;
   float a[32];
-  // step 1 (xor 16): keep half [0,32) or [32,64)
   {
     const bool up = lane & 16;
 #pragma unroll
@@ -164,48 +192,18 @@ __device__ __forceinline__ float2 warp_colsum64(const float (&v)[64]) {
       a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
   }
-  float b[16];
-  {
-    const bool up = lane & 8;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float send = up ? a[j] : a[16 + j];
-      const float keep = up ? a[16 + j] : a[j];
-      b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  for (int w = 32, bit = 8; w >= 4; w /= 2, bit /= 2) {
+    const bool up = lane & bit;
+#pragma unroll
+    for (int j = 0; j < w / 2; ++j) {
+      const float send = up ? a[j] : a[w / 2 + j];
+      const float keep = up ? a[w / 2 + j] : a[j];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
     }
   }
-  float c[8];
-  {
-    const bool up = lane & 4;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float send = up ? b[j] : b[8 + j];
-      const float keep = up ? b[8 + j] : b[j];
-      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-  }
-  float d[4];
-  {
-    const bool up = lane & 2;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float send = up ? c[j] : c[4 + j];
-      const float keep = up ? c[4 + j] : c[j];
-      d[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-  }
-  float e[2];
-  {
-    const bool up = lane & 1;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const float send = up ? d[j] : d[2 + j];
-      const float keep = up ? d[2 + j] : d[j];
-      e[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-    }
-  }
-  // lane bits (16,8,4,2,1) selected halves 32,16,8,4,2: column base = 32*b4 + 16*b3 + 8*b2 + 4*b1 + 2*b0
-  return make_float2(e[0], e[1]);
+  // lane bits (16,8,4,2,1) selected halves 32,16,8,4,2 -> columns colsum_base(lane) + {0, 1}
+  return make_float2(a[0], a[1]);
 }
 
 __device__ __forceinline__ int colsum_base(int lane) {
@@ -213,7 +211,7 @@ __device__ __forceinline__ int colsum_base(int lane) {
          2 * (lane & 1);
 }
 
-template <int MODE>
+template <int MODE, bool PROF>
 __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(TcBwdArgs a) {
   using Cfg = TcBwdCfg;
   constexpr int H = Cfg::H;
@@ -233,10 +231,9 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   uint64_t* st_empty = st_full + Cfg::NSTAGE;     // [2][NSTAGE]: split by use parity so a producer
                                                   // running a whole job ahead cannot alias a phase
   uint64_t* dw_full = st_empty + 2 * Cfg::NSTAGE; // [1]
-  uint64_t* dw_empty = dw_full + 1;               // [1]
+  uint64_t* dw_empty = dw_full + 1;               // [1], count 8 (epilogue warps)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(dw_empty + 1);
   float* dbp = reinterpret_cast<float*>(smem + Cfg::OFF_DBP);
-  float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
   float* sbias = reinterpret_cast<float*>(smem + Cfg::OFF_BIAS);
 
   const int warp = threadIdx.x / 32;
@@ -264,7 +261,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       ptx::mbar_init(&st_empty[Cfg::NSTAGE + s], 1);
     }
     ptx::mbar_init(dw_full, 1);
-    ptx::mbar_init(dw_empty, 4);
+    ptx::mbar_init(dw_empty, 8);
     ptx::fence_mbarrier_init();
   }
   for (int i = threadIdx.x; i < (K + 2) * H; i += blockDim.x)
@@ -275,6 +272,12 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_base_slot;
 
+  // Register budget per warpgroup: the CTA pool is fixed at launch (384 x 168);
+  // setmaxnreg moves registers from the control warpgroup to the epilogue.
+  static_assert(256 * 224 + 128 * 56 <= Cfg::THREADS * 168, "setmaxnreg exceeds the CTA register pool");
+  if (warp < 8) ptx::regs_inc<224>();
+  else ptx::regs_dec<56>();
+
   if (warp < 8) {
     // ================================================================ epilogue
     const int g = warp / 4;
@@ -283,41 +286,118 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     const uint32_t t_ahi = tmem + g * Cfg::SLOT_COLS + lane_off;
     const uint32_t t_alo = t_ahi + H;
     const uint32_t t_d = t_ahi + 2 * H;
+    const uint32_t t_dw = tmem + Cfg::DW_COL + lane_off;
     float4* scr = reinterpret_cast<float4*>(a.scratch) + ((int64_t)blockIdx.x * 2 + g) * K * 16 * 128;
     float* scr_inv = a.scratch + (int64_t)gridDim.x * 2 * K * 16 * 128 * 4 + ((int64_t)blockIdx.x * 2 + g) * K * 128;
+    float* gpart0 = a.grad_partial + (int64_t)blockIdx.x * 2 * n_par;  // hh + hl, db
+    float* gpart1 = gpart0 + n_par;                                    // lh
     const int trow = 32 * wq + lane;  // row inside the tile
     uint32_t pe = 0, pd = 0;
     int64_t job = 0;                  // global dW job counter (all pairs)
+
+    // Drain the dW accumulator of global job jf: this warp reads its TMEM lane
+    // quarter, column half g. Lanes < 64 hold (h_hi row i) x [d_hi | d_lo]:
+    // hh + hl; lanes >= 64 hold (h_lo row i - 64) x d_hi: lh.
+    auto flush = [&](int64_t jf) {
+      const int jj = (int)(jf % n_dw);
+      const int lin = jj <= K ? K + 1 - jj : 0;
+      const int rowbase = jj <= K ? 0 : (jj - K - 1) * H;
+      const bool with_db = jj <= K + 1;
+      ptx::mbar_wait(dw_full, (uint32_t)(jf & 1));
+      ptx::tc_fence_after();
+      const int c0 = 32 * g;
+      float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow) * H + c0
+                         : gpart1 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow - 64) * H + c0;
+      float p0[16], p1[16];
+      ptx::tmem_ld16(t_dw + c0, p0);
+      ptx::tmem_ld16(t_dw + c0 + 16, p1);
+      if (wq < 2) {
+        float q0[16], q1[16];
+        ptx::tmem_ld16(t_dw + 64 + c0, q0);
+        ptx::tmem_ld16(t_dw + 64 + c0 + 16, q1);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          p0[j] += q0[j];
+          p1[j] += q1[j];
+        }
+      } else {
+        ptx::tmem_wait_ld();
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(dw_empty);  // this warp's part of the accumulator is read
+      float4* g4 = reinterpret_cast<float4*>(gw);
+      float4 gv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) gv[j] = __ldcg(g4 + j);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __stcg(g4 + j, make_float4(gv[j].x + p0[4 * j], gv[j].y + p0[4 * j + 1], gv[j].z + p0[4 * j + 2],
+                                   gv[j].w + p0[4 * j + 3]));
+        __stcg(g4 + 4 + j, make_float4(gv[4 + j].x + p1[4 * j], gv[4 + j].y + p1[4 * j + 1],
+                                       gv[4 + j].z + p1[4 * j + 2], gv[4 + j].w + p1[4 * j + 3]));
+      }
+      if (with_db && warp < 2) {  // bias gradient: fixed-order sum of the 8 warp partials
+        const float* db = dbp + (jf % 3) * 8 * 64 + trow;
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += db[w * 64];
+        gpart0[mlp_b_offset(lin, in_dim, H) + trow] += s;
+      }
+    };
+    // The previous job's dW must be drained first: this job's staging ring
+    // slots are only released by dW MMAs that accumulate onto it.
+    auto stage_chunk = [&](const float (&hin)[H], const float (&d)[H]) {
+      if (job >= 1) flush(job - 1);
+      const int64_t gi = job * 8 + warp;  // staging chunk counter
+      stage_acquire(st_empty, gi);
+      uint8_t* sb = stage + (size_t)(gi % Cfg::NSTAGE) * Cfg::STAGE_BYTES;
+      stage_row(sb, lane, hin);
+      stage_row(sb + 16384, lane, d);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&st_full[gi % Cfg::NSTAGE]);
+    };
+    auto write_db = [&](const float (&d)[H]) {
+      const float2 cs = warp_colsum64(d);
+      float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
+      dst[0] = cs.x;
+      dst[1] = cs.y;
+    };
+    auto wait_dx = [&]() {
+      ptx::mbar_wait(&d_full[g], pd);
+      pd ^= 1;
+      ptx::tc_fence_after();
+    };
+
     for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
       const int64_t row = (2 * pair + g) * 128 + trow;
       const bool valid = row < a.n_rows;
       float h[H];
       // ---------------------------------------------- forward recompute
-      {
-        float v[H];
-        for (int c = 0; c < nseg; ++c) {
-          if (c > 0) {
-            ptx::mbar_wait(&a_empty[g], pe);
-            pe ^= 1;
-            ptx::tc_fence_after();
-          }
-          bwd_gather<MODE>(a, row, valid, c, v);
-          tc_store_a<H>(t_ahi, t_alo, v);
-          tc_signal(&a_full[g]);
+      for (int c = 0; c < nseg; ++c) {
+        if (c > 0) {
+          ptx::mbar_wait(&a_empty[g], pe);
+          pe ^= 1;
+          ptx::tc_fence_after();
         }
+        bwd_gather<MODE>(a, row, valid, c, h);
+        bwd_store_a(t_ahi, t_alo, h);
+        tc_signal(&a_full[g]);
       }
       ptx::mbar_wait(&d_full[g], pd);
       pd ^= 1;
       ptx::tc_fence_after();
-      tc_load_d<H>(t_d, sbias, h);
+      bwd_load_d(t_d, sbias, h);
       for (int l = 1; l <= K; ++l) {
-        tc_store_a<H>(t_ahi, t_alo, h);
+        bwd_store_a(t_ahi, t_alo, h);
         tc_signal(&a_full[g]);
         ptx::mbar_wait(&d_full[g], pd);
         pd ^= 1;
         ptx::tc_fence_after();
         float u[H];
-        tc_load_d<H>(t_d, sbias + l * H, u);
+        bwd_load_d(t_d, sbias + l * H, u);
         const float inv_std = ln0_tree<H>(u);
         float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
 #pragma unroll
@@ -328,9 +408,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       }
       // ---------------------------------------------- backward
       float dh[H];
-      // output adjoint d_y (model.cpp:354-360 folded in for the edge MLP)
       if (valid) {
-        if (MODE == kEdgeInput) {
+        if (MODE == kEdgeInput) {  // d_y = de + inv_d * d_a[dst] (model.cpp:354-360)
           const float s = __ldg(a.inv_deg + row);
           const float4* da = reinterpret_cast<const float4*>(a.d_a + (int64_t)__ldg(a.dst + row) * H);
           const float4* de = reinterpret_cast<const float4*>(a.de_io + row * H);
@@ -357,46 +436,25 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
 #pragma unroll
         for (int j = 0; j < H; ++j) dh[j] = 0.f;
       }
-      // one backward step: d (this linear's output adjoint) is in dh; hin is
-      // the linear's input (residual stream) -> stage, A <- d, dX via MMA.
-      auto publish = [&](const float (&d)[H], const float (&hin)[H], bool with_db) {
-        tc_store_a<H>(t_ahi, t_alo, d);
-        tc_signal(&a_full[g]);
-        if (with_db) {
-          const float2 cs = warp_colsum64(d);
-          float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
-          dst[0] = cs.x;
-          dst[1] = cs.y;
-        }
-        const int64_t gi = job * 8 + warp;  // staging chunk counter
-        stage_acquire(st_empty, gi);
-        const int buf = (int)(gi % Cfg::NSTAGE);
-        uint8_t* sb = stage + (size_t)buf * Cfg::STAGE_BYTES;
-        stage_row(sb, lane, hin);
-        stage_row(sb + 16384, lane, d);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&st_full[buf]);
-      };
-      // output projection: dW_out += h_k^T d_y, d_h = d_y W_out^T
-      publish(dh, h, true);
+      // output projection (nn.cpp:241-245): dX = d_y W_out^T, dW_out += h_k^T d_y
+      bwd_store_a(t_ahi, t_alo, dh);
+      tc_signal(&a_full[g]);
+      write_db(dh);
+      stage_chunk(h, dh);
+      wait_dx();
       ++job;
-      ptx::mbar_wait(&d_full[g], pd);
-      pd ^= 1;
-      ptx::tc_fence_after();
-      tc_load_raw<H>(t_d, dh);
-      // residual blocks in reverse (nn.cpp:259-274). The residual term of
-      // d_prev = d_u W^T + d_h is folded into the MMA by pre-loading D with d_h.
+      bwd_load_d(t_d, nullptr, dh);
+      // residual blocks in reverse (nn.cpp:259-274)
       for (int l = K; l >= 1; --l) {
         const float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
         const float inv_std = scr_inv[(l - 1) * 128 + trow];
-        tc_store_raw<H>(t_d, dh);
+        bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
         float p1[8], p2[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float4 t4 = st[q * 128];
+          const float4 t4 = ld_reload(st + q * 128);
           const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -416,85 +474,84 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float4 t4 = st[q * 128];
+          const float4 t4 = ld_reload(st + q * 128);
           dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
           dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
           dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
           dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
         }
-        publish(dh, h, true);
+        bwd_store_a(t_ahi, t_alo, dh);
+        tc_signal(&a_full[g]);
+        write_db(dh);
+        stage_chunk(h, dh);
+        wait_dx();
         ++job;
-        ptx::mbar_wait(&d_full[g], pd);
-        pd ^= 1;
-        ptx::tc_fence_after();
-        tc_load_raw<H>(t_d, dh);
+        bwd_load_d(t_d, nullptr, dh);  // d_prev = d_u W^T + d_h
       }
       // input projection (nn.cpp:277-281): per segment c, dW0[seg c] and d_in[seg c]
-      tc_store_a<H>(t_ahi, t_alo, dh);
+      bwd_store_a(t_ahi, t_alo, dh);
       tc_signal(&a_full[g]);
-      {
-        const float2 cs = warp_colsum64(dh);
-        float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
-        dst[0] = cs.x;
-        dst[1] = cs.y;
-      }
+      write_db(dh);
       for (int c = 0; c < nseg; ++c) {
-        {
-          float xin[H];
-          bwd_gather<MODE>(a, row, valid, c, xin);
-          const int64_t gi = job * 8 + warp;
-          stage_acquire(st_empty, gi);
-          const int buf = (int)(gi % Cfg::NSTAGE);
-          uint8_t* sb = stage + (size_t)buf * Cfg::STAGE_BYTES;
-          stage_row(sb, lane, xin);
-          stage_row(sb + 16384, lane, dh);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&st_full[buf]);
-        }
+        bwd_gather<MODE>(a, row, valid, c, h);
+        stage_chunk(h, dh);
+        wait_dx();
         ++job;
-        ptx::mbar_wait(&d_full[g], pd);
-        pd ^= 1;
-        ptx::tc_fence_after();
         float* outp;
         if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
         else outp = c == 0 ? a.d_a_out : a.d_x_out;
         float4* o = reinterpret_cast<float4*>(outp + row * H);
 #pragma unroll
-        for (int cc = 0; cc < H; cc += 32) {
-          float p[32];
-          ptx::tmem_ld32(t_d + cc, p);
+        for (int cc = 0; cc < H; cc += 16) {
+          float p[16];
+          ptx::tmem_ld16(t_d + cc, p);
           ptx::tmem_wait_ld();
           if (valid) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o[cc / 4 + j] = make_float4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+            for (int j = 0; j < 4; ++j) o[cc / 4 + j] = make_float4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
           }
         }
         if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays
       }
     }
+    if (job >= 1) flush(job - 1);  // last dW job of this CTA
   } else if (warp == 8) {
     // ================================================================ MMA issuer
     if (lane == 0) {
+      // fresh copy of the TMEM base: the shared prologue value may live in a spill slot
+      const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(tmem_base_slot);
       constexpr uint32_t idesc = ptx::idesc_tf32(128, H);
       constexpr uint32_t idesc_dw = ptx::idesc_tf32(128, 2 * H) | (1u << 15) | (1u << 16);  // A, B MN-major
       int ws = 0;
       uint32_t wph = 0, pa[2] = {0, 0}, pdw = 0;
       int64_t gi = 0;  // staging chunk counter
       auto mma3 = [&](int s, uint32_t bbase, bool first_zero) {
-        const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+        const uint32_t slot = ptx::opaque(tm + s * Cfg::SLOT_COLS);
+        // descriptor start addresses advance in 16-byte units: bump the encoded
+        // base instead of re-encoding (keeps the issuer's register use small)
+        const uint64_t d0 = ptx::opaque64(ptx::smem_desc(bbase, Cfg::LBO, Cfg::SBO));
 #pragma unroll
         for (int ks = 0; ks < H / 8; ++ks) {
-          const uint32_t kb = bbase + ks * 2 * Cfg::LBO;
-          const uint64_t b_hi = ptx::smem_desc(kb, Cfg::LBO, Cfg::SBO);
-          const uint64_t b_lo = ptx::smem_desc(kb + Cfg::LO_OFF, Cfg::LBO, Cfg::SBO);
+          const uint64_t b_hi = d0 + (uint64_t)((ks * 2 * Cfg::LBO) >> 4);
+          const uint64_t b_lo = b_hi + (uint64_t)(Cfg::LO_OFF >> 4);
           ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (!first_zero || ks > 0) ? 1u : 0u);
           ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
           ptx::mma_tf32_ts(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
         }
       };
+      unsigned long long pc_w = 0, pc_a = 0, pc_st = 0, pc_dw = 0;  // wait cycles (profiling only)
+      const long long t_start = clock64();
+      auto timed_wait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+        if (!PROF) {
+          ptx::mbar_wait(bar, par);
+          return;
+        }
+        const long long t0 = clock64();
+        ptx::mbar_wait(bar, par);
+        acc += (unsigned long long)(clock64() - t0);
+      };
       auto next_w = [&]() -> uint32_t {
-        ptx::mbar_wait(&w_full[ws], wph);
+        timed_wait(&w_full[ws], wph, pc_w);
         ptx::tc_fence_after();
         return ptx::smem_u32(wring + (size_t)ws * Cfg::CHUNK_FLOATS);
       };
@@ -505,23 +562,27 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           wph ^= 1;
         }
       };
+      unsigned long long pc_fwd = 0, pc_dwt = 0, pc_mma = 0;  // phase cycles (profiling only)
       auto dw_job = [&]() {
-        ptx::mbar_wait(dw_empty, pdw ^ 1);
+        const long long t_dw0 = PROF ? clock64() : 0;
+        timed_wait(dw_empty, pdw ^ 1, pc_dw);
         ptx::tc_fence_after();
         for (int b = 0; b < 8; ++b, ++gi) {
           const int buf = (int)(gi % Cfg::NSTAGE);
           const uint32_t par = (uint32_t)((gi / Cfg::NSTAGE) & 1);
-          ptx::mbar_wait(&st_full[buf], par);
+          timed_wait(&st_full[buf], par, pc_st);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(stage + (size_t)buf * Cfg::STAGE_BYTES);
+          constexpr uint64_t swz = (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+          const uint64_t a0 = ptx::opaque64(ptx::smem_desc(sa, Cfg::ST_LBO, Cfg::ST_SBO) | swz);
+          const uint32_t t_dw = ptx::opaque(tm + Cfg::DW_COL);
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            constexpr uint64_t swz = (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
-            const uint64_t ad = ptx::smem_desc(sa + ks * 2 * Cfg::ST_SBO, Cfg::ST_LBO, Cfg::ST_SBO) | swz;
-            const uint64_t bd = ptx::smem_desc(sa + 16384 + ks * 2 * Cfg::ST_SBO, Cfg::ST_LBO, Cfg::ST_SBO) | swz;
+            const uint64_t ad = a0 + (uint64_t)((ks * 2 * Cfg::ST_SBO) >> 4);
+            const uint64_t bd = ad + (uint64_t)(16384 >> 4);
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + Cfg::DW_COL),
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(t_dw),
                 "l"(ad), "l"(bd), "r"(idesc_dw), "r"((b > 0 || ks > 0) ? 1u : 0u)
                 : "memory");
           }
@@ -529,13 +590,15 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         }
         ptx::mma_commit(dw_full);
         pdw ^= 1;
+        if (PROF) pc_dwt += (unsigned long long)(clock64() - t_dw0);
       };
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+        const long long t_p0 = PROF ? clock64() : 0;
         // forward recompute: input chunks then hidden blocks (no output linear)
         for (int c = 0; c < nseg; ++c) {
           const uint32_t bb = next_w();
           for (int s = 0; s < 2; ++s) {
-            ptx::mbar_wait(&a_full[s], pa[s]);
+            timed_wait(&a_full[s], pa[s], pc_a);
             pa[s] ^= 1;
             ptx::tc_fence_after();
             mma3(s, bb, c == 0);
@@ -546,7 +609,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         for (int l = 1; l <= K; ++l) {
           const uint32_t bb = next_w();
           for (int s = 0; s < 2; ++s) {
-            ptx::mbar_wait(&a_full[s], pa[s]);
+            timed_wait(&a_full[s], pa[s], pc_a);
             pa[s] ^= 1;
             ptx::tc_fence_after();
             mma3(s, bb, true);
@@ -554,16 +617,19 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           }
           release_w();
         }
+        if (PROF) pc_fwd += (unsigned long long)(clock64() - t_p0);
         // backward: output linear, hidden blocks in reverse (dX then dW each);
         // hidden steps accumulate onto D pre-loaded with the residual d_h
         for (int step = 0; step <= K; ++step) {
           const uint32_t bb = next_w();
           for (int s = 0; s < 2; ++s) {
-            ptx::mbar_wait(&a_full[s], pa[s]);
+            timed_wait(&a_full[s], pa[s], pc_a);
             pa[s] ^= 1;
             ptx::tc_fence_after();
+            const long long t_m0 = PROF ? clock64() : 0;
             mma3(s, bb, step == 0);
             ptx::mma_commit(&d_full[s]);
+            if (PROF) pc_mma += (unsigned long long)(clock64() - t_m0);
           }
           release_w();
           dw_job();
@@ -572,7 +638,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         for (int c = 0; c < nseg; ++c) {
           const uint32_t bb = next_w();
           for (int s = 0; s < 2; ++s) {
-            ptx::mbar_wait(&a_full[s], pa[s]);
+            timed_wait(&a_full[s], pa[s], pc_a);
             pa[s] ^= 1;
             ptx::tc_fence_after();
             mma3(s, bb, true);
@@ -582,9 +648,19 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           dw_job();
         }
       }
+      if (PROF) {
+        atomicAdd(a.prof + kProfTotal, (unsigned long long)(clock64() - t_start));
+        atomicAdd(a.prof + kProfW, pc_w);
+        atomicAdd(a.prof + kProfA, pc_a);
+        atomicAdd(a.prof + kProfSt, pc_st);
+        atomicAdd(a.prof + kProfDwE, pc_dw);
+        atomicAdd(a.prof + kProfFwd, pc_fwd);
+        atomicAdd(a.prof + kProfDw, pc_dwt);
+        atomicAdd(a.prof + kProfMma, pc_mma);
+      }
     }
-  } else if (warp == 9 || warp == 10 || warp == 11) {
-    // ================================================================ loader
+  } else {
+    // ================================================================ loader (warp 9; 10-11 idle)
     if (warp == 9 && lane == 0) {
       int ws = 0;
       uint32_t wph = 0;
@@ -599,66 +675,6 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             wph ^= 1;
           }
         }
-      }
-    }
-  } else {
-    // ================================================================ dW flush (warps 12-15)
-    const int wq = warp % 4;
-    const int L = 32 * wq + lane;  // TMEM lane owned
-    const uint32_t t_dw = tmem + Cfg::DW_COL + ((uint32_t)(32 * wq) << 16);
-    float* gpart = a.grad_partial + (int64_t)blockIdx.x * n_par;
-    uint32_t pdw = 0;
-    int64_t job = 0;
-    for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
-      for (int jj = 0; jj < n_dw; ++jj, ++job) {
-        // which linear / rows this job covers
-        int lin, rowbase;
-        bool with_db;
-        if (jj <= K) {
-          lin = K + 1 - jj;  // out (K+1), then K..1
-          rowbase = 0;
-          with_db = true;
-        } else {
-          lin = 0;
-          rowbase = (jj - K - 1) * H;
-          with_db = jj == K + 1;
-        }
-        ptx::mbar_wait(dw_full, pdw);
-        pdw ^= 1;
-        ptx::tc_fence_after();
-        float* gw = gpart + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + (L & 63)) * H;
-#pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          float p[32];
-          ptx::tmem_ld32(t_dw + c, p);
-          ptx::tmem_wait_ld();
-          if (L < 64) {
-            float q[32];
-            ptx::tmem_ld32(t_dw + 64 + c, q);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) p[j] += q[j];  // hh + hl
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) xch[(L - 64) * 33 + j] = p[j];  // lh
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (L < 64) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) gw[c + j] += p[j] + xch[L * 33 + j];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-        }
-        ptx::tc_fence_before();
-        if (lane == 0) ptx::mbar_arrive(dw_empty);  // accumulator may be overwritten now
-        if (L < 64 && with_db) {
-          const float* db = dbp + (job % 3) * 8 * 64;
-          float sdb = 0.f;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) sdb += db[w * 64 + L];
-          gpart[mlp_b_offset(lin, in_dim, H) + L] += sdb;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
     }
   }

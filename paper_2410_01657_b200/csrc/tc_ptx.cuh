@@ -30,17 +30,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
-// try_wait with a suspend-time hint: the thread sleeps until the phase
-// completes (or the hint expires) instead of spinning on issue slots.
+// try_wait: the hardware suspends the thread for a short, system-defined time
+// when the phase is incomplete. (An explicit suspend-time hint compiles to a
+// NANOSLEEP of that length and adds up to the full hint per failed probe.)
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
+
 // Watchdog: a wait that does not complete within ~20 s of SM clock reports
 // the barrier and traps, so a protocol bug fails the launch instead of
 // hanging the device.
@@ -114,6 +116,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
       : "r"(taddr)
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
   asm volatile(
@@ -163,6 +174,25 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)1 << 46;  // version
   return d;                // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE
 }
+
+// fp32 -> tf32 by truncation (one LOP3): hi = x with the 13 low mantissa bits
+// cleared; x - hi is exact in fp32 and |x - hi| < 2^-10 |x|, so the 3xTF32
+// split hi*hi + hi*lo + lo*hi keeps ~2^-20 relative accuracy per product.
+// Value barrier: the compiler cannot hoist or rematerialise expressions derived
+// from the result (keeps single-thread MMA issuers from spilling hoisted
+// address constants).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+__device__ __forceinline__ uint64_t opaque64(uint64_t x) {
+  uint64_t r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(x));
+  return r;
+}
+
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 // fp32 -> tf32 (round to nearest, ties away), result kept in fp32 format.
 __device__ __forceinline__ float tf32_rna(float x) {
