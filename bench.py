@@ -302,7 +302,8 @@ def main():
                 "frac": achieved / tf32_peak, "traffic": traffic, "kernel": dom,
                 "peak_basis": "dense TF32 = 1/2 of measured sustained bf16 (MEASURED_PEAKS.json)",
                 "flops_per_launch": flops[dom], "ms_per_launch": avg_ms,
-                "pipe": "fp32 SIMT (v1 kernels; tcgen05 path pending)"}
+                "pipe": ("tcgen05 kind::tf32 3xTF32 (3 tensor products per algorithmic product; the backward "
+                         "kernel also recomputes the forward: algorithmic flops exclude both)")}
 
     # ---- e2e through the public C-ABI with host buffers
     e2e = None

@@ -103,6 +103,10 @@ __device__ __forceinline__ float4 ld_reload(const float4* p) {
   return v;
 }
 
+__device__ __forceinline__ void red_add4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // A <- [hi | lo] split of v, 16 columns at a time (low register pressure).
 __device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const float (&v)[64]) {
 #pragma unroll
@@ -327,23 +331,21 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(dw_empty);  // this warp's part of the accumulator is read
-      float4* g4 = reinterpret_cast<float4*>(gw);
-      float4 gv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) gv[j] = __ldcg(g4 + j);
+      // Fire-and-forget vector reductions into this CTA's partial: every
+      // element has a single owning thread, so the adds land in program order
+      // (deterministic) and no load latency is exposed.
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        __stcg(g4 + j, make_float4(gv[j].x + p0[4 * j], gv[j].y + p0[4 * j + 1], gv[j].z + p0[4 * j + 2],
-                                   gv[j].w + p0[4 * j + 3]));
-        __stcg(g4 + 4 + j, make_float4(gv[4 + j].x + p1[4 * j], gv[4 + j].y + p1[4 * j + 1],
-                                       gv[4 + j].z + p1[4 * j + 2], gv[4 + j].w + p1[4 * j + 3]));
+        red_add4(gw + 4 * j, p0[4 * j], p0[4 * j + 1], p0[4 * j + 2], p0[4 * j + 3]);
+        red_add4(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3]);
       }
       if (with_db && warp < 2) {  // bias gradient: fixed-order sum of the 8 warp partials
         const float* db = dbp + (jf % 3) * 8 * 64 + trow;
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += db[w * 64];
-        gpart0[mlp_b_offset(lin, in_dim, H) + trow] += s;
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(s)
+                     : "memory");
       }
     };
     // The previous job's dW must be drained first: this job's staging ring
