@@ -183,10 +183,13 @@ enum {
 };
 int hgnn_kernel_timing(hgnn_ctx* ctx, int enable);
 int hgnn_kernel_time(hgnn_ctx* ctx, int kernel_class, double* total_ms, int64_t* launches);
-/* Wait-cycle counters of the tensor-core backward kernel (after
- * hgnn_set_option(ctx, "bwd_profile", 1)): [edge 8][node 8] = total, weight,
- * A-operand, staging, dW-drain waits of the MMA issuer; flush wait, flush work. */
-int hgnn_debug_profile(hgnn_ctx* ctx, uint64_t* out16);
+/* Cycle counters of the tensor-core kernels (after hgnn_set_option(ctx,
+ * "bwd_profile", 1); debugging aid, summed over CTAs):
+ *   [0..8)   backward, edge MLP  (kProf* in mlp_tc_bwd.cuh)
+ *   [8..16)  backward, node MLP
+ *   [16..24) forward, edge MLP   (kFwdProf* in mlp_tc.cuh)
+ *   [24..32) forward, node MLP */
+int hgnn_debug_profile(hgnn_ctx* ctx, uint64_t* out32);
 /* Own-kernel launches issued since the last reset (for gpu_launches). */
 int64_t hgnn_launch_count(hgnn_ctx* ctx, int reset);
 /* Bytes handed to NCCL by this rank since the last reset (CommCounters analogue). */

@@ -505,11 +505,12 @@ bool use_tc(const hgnn_ctx* c) { return c->fwd_impl == 1 && tc_eligible(c); }
 template <int H, int MODE>
 void launch_tc_typed(hgnn_ctx* c, const TcFwdArgs& args) {
   using Cfg = TcCfg<H>;
-  auto k = mlp_tc_forward_kernel<H, MODE>;
-  static bool attr = false;
-  if (!attr) {
+  const bool prof = args.prof != nullptr;
+  auto k = prof ? mlp_tc_forward_kernel<H, MODE, true> : mlp_tc_forward_kernel<H, MODE, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[prof]) {
     CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
-    attr = true;
+    attr[prof] = true;
   }
   const int64_t pairs = ((args.n_rows + 127) / 128 + 1) / 2;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
@@ -532,6 +533,7 @@ void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const f
   args.chunks = c->chunks.p + c->chunk_off[(size_t)(2 * m + (edge ? 0 : 1))];
   args.params = layer_params(c, m, edge).p;
   args.k = (int)c->K;
+  args.prof = c->prof_on ? c->prof.p + 2 * kProfCount + (edge ? 0 : kProfCount) : nullptr;
   if (c->H == 64) {
     if (edge) launch_tc_typed<64, kEdgeInput>(c, args);
     else launch_tc_typed<64, kNodeInput>(c, args);
@@ -1137,8 +1139,8 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_forward_impl: 0 (simt) or 1 (tcgen05)");
       c->fwd_impl = (int)value;
     } else if (k == "bwd_profile") {
-      c->prof.alloc(2 * kProfCount);
-      CUDA_OK(cudaMemsetAsync(c->prof.p, 0, sizeof(unsigned long long) * 2 * kProfCount, c->stream));
+      c->prof.alloc(4 * kProfCount);
+      CUDA_OK(cudaMemsetAsync(c->prof.p, 0, sizeof(unsigned long long) * 4 * kProfCount, c->stream));
       c->prof_on = value != 0;
     } else if (k == "mlp_backward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
@@ -1174,11 +1176,11 @@ int hgnn_kernel_time(hgnn_ctx* c, int cls, double* total_ms, int64_t* launches) 
   });
 }
 
-int hgnn_debug_profile(hgnn_ctx* c, uint64_t* out16) {
+int hgnn_debug_profile(hgnn_ctx* c, uint64_t* out32) {
   return guarded([&] {
     bind(c);
     if (!c->prof.p) fail(HGNN_ERR_UNINITIALIZED, "bwd_profile not enabled");
-    CUDA_OK(cudaMemcpy(out16, c->prof.p, sizeof(unsigned long long) * 2 * kProfCount, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(out32, c->prof.p, sizeof(unsigned long long) * 4 * kProfCount, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -56,7 +56,13 @@ struct TcFwdArgs {
   const float* chunks;  // (nseg + k + 1) chunks in MMA order
   const float* params;  // fp32 for_each layout (biases)
   int k;
+  unsigned long long* prof;  // optional cycle counters (kFwdProf*), PROF instantiation only
 };
+
+// Optional instrumentation of the forward kernel (cycles summed over CTAs;
+// epilogue figures from warp 0 lane 0).
+enum { kFwdProfIssTotal = 0, kFwdProfIssA = 1, kFwdProfIssW = 2, kFwdProfIssMma = 3, kFwdProfEpiTotal = 4,
+       kFwdProfEpiD = 5, kFwdProfEpiAE = 6, kFwdProfEpiSig = 7 };
 
 __device__ __forceinline__ float elu_fast(float z) { return z > 0.f ? z : __expf(z) - 1.0f; }
 
@@ -148,7 +154,7 @@ __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool 
   }
 }
 
-template <int H, int MODE>
+template <int H, int MODE, bool PROF>
 __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(TcFwdArgs a) {
   using Cfg = TcCfg<H>;
   constexpr int nseg = MODE == kEdgeInput ? 3 : 2;
@@ -203,6 +209,20 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     const uint32_t t_alo = t_ahi + H;
     const uint32_t t_d = t_ahi + 2 * H;
     uint32_t pe = 0, pd = 0;
+    unsigned long long e_d = 0, e_ae = 0, e_sig = 0;
+    const long long e_t0 = PROF ? clock64() : 0;
+    auto wait_d = [&]() {
+      const long long t0 = PROF ? clock64() : 0;
+      ptx::mbar_wait(&d_full[g], pd);
+      pd ^= 1;
+      ptx::tc_fence_after();
+      if (PROF) e_d += (unsigned long long)(clock64() - t0);
+    };
+    auto signal_a = [&]() {
+      const long long t0 = PROF ? clock64() : 0;
+      tc_signal(&a_full[g]);
+      if (PROF) e_sig += (unsigned long long)(clock64() - t0);
+    };
     float v[H];
     int64_t pair = blockIdx.x;
     if (pair < n_pairs) {
@@ -216,25 +236,23 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       // input projection: nseg K-chunks streamed through A, next one prefetched
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
+          const long long t0 = PROF ? clock64() : 0;
           ptx::mbar_wait(&a_empty[g], pe);
           pe ^= 1;
           ptx::tc_fence_after();
+          if (PROF) e_ae += (unsigned long long)(clock64() - t0);
         }
         tc_store_a<H>(t_ahi, t_alo, v);
-        tc_signal(&a_full[g]);
+        signal_a();
         if (c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v);
       }
-      ptx::mbar_wait(&d_full[g], pd);
-      pd ^= 1;
-      ptx::tc_fence_after();
+      wait_d();
       tc_load_d<H>(t_d, sbias, h);
       // residual blocks
       for (int l = 1; l <= a.k; ++l) {
         tc_store_a<H>(t_ahi, t_alo, h);
-        tc_signal(&a_full[g]);
-        ptx::mbar_wait(&d_full[g], pd);
-        pd ^= 1;
-        ptx::tc_fence_after();
+        signal_a();
+        wait_d();
         float u[H];
         tc_load_d<H>(t_d, sbias + l * H, u);
         ln0_tree<H>(u);
@@ -243,15 +261,13 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       }
       // output projection; the next tile's first segment is gathered meanwhile
       tc_store_a<H>(t_ahi, t_alo, h);
-      tc_signal(&a_full[g]);
+      signal_a();
       const int64_t next = pair + gridDim.x;
       if (next < n_pairs) {
         const int64_t nrow = (2 * next + g) * 128 + 32 * wq + lane;
         tc_gather<H, MODE>(a, nrow, nrow < a.n_rows, 0, v);
       }
-      ptx::mbar_wait(&d_full[g], pd);
-      pd ^= 1;
-      ptx::tc_fence_after();
+      wait_d();
       {  // stream y = D + b straight to global, 32 columns at a time
         const float* bo = sbias + (a.k + 1) * H;
         float4* o = reinterpret_cast<float4*>(a.out + row * H);
@@ -269,42 +285,67 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         }
       }
     }
+    if (PROF && warp == 0 && lane == 0) {
+      atomicAdd(a.prof + kFwdProfEpiTotal, (unsigned long long)(clock64() - e_t0));
+      atomicAdd(a.prof + kFwdProfEpiD, e_d);
+      atomicAdd(a.prof + kFwdProfEpiAE, e_ae);
+      atomicAdd(a.prof + kFwdProfEpiSig, e_sig);
+    }
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // warp-uniform TMEM base (uniform registers; no per-MMA waterfall loop)
+    const uint32_t tm = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t*>(tmem_base_slot), 0);
+    {  // all 32 lanes run the schedule; mma/commit elect one lane
       constexpr uint32_t idesc = ptx::idesc_tf32(128, H);
       int ws = 0;
       uint32_t wph = 0, pa[2] = {0, 0};
+      unsigned long long i_a = 0, i_w = 0, i_m = 0;
+      const long long i_t0 = PROF ? clock64() : 0;
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
         for (int j = 0; j < n_chunks; ++j) {
           const int l = j < nseg ? 0 : j - nseg + 1;
           const int c = j < nseg ? j : 0;
           const bool last_chunk = (l > 0) || (c == nseg - 1);
+          long long t0 = PROF ? clock64() : 0;
           ptx::mbar_wait(&w_full[ws], wph);
           ptx::tc_fence_after();
+          if (PROF) i_w += (unsigned long long)(clock64() - t0);
           const uint32_t bbase = ptx::smem_u32(wring + (size_t)ws * Cfg::CHUNK_FLOATS);
           for (int s = 0; s < 2; ++s) {
+            if (PROF) t0 = clock64();
             ptx::mbar_wait(&a_full[s], pa[s]);
             pa[s] ^= 1;
             ptx::tc_fence_after();
-            const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+            if (PROF) {
+              const long long t1 = clock64();
+              i_a += (unsigned long long)(t1 - t0);
+              t0 = t1;
+            }
+            const uint32_t slot = ptx::opaque(tm + s * Cfg::SLOT_COLS);
+            const uint64_t d0 = ptx::opaque64(ptx::smem_desc(bbase, Cfg::LBO, Cfg::SBO));
 #pragma unroll
             for (int ks = 0; ks < H / 8; ++ks) {
-              const uint32_t kb = bbase + ks * 2 * Cfg::LBO;
-              const uint64_t b_hi = ptx::smem_desc(kb, Cfg::LBO, Cfg::SBO);
-              const uint64_t b_lo = ptx::smem_desc(kb + Cfg::LO_OFF, Cfg::LBO, Cfg::SBO);
-              ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-              ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
-              ptx::mma_tf32_ts(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
+              const uint64_t b_hi = d0 + (uint64_t)((ks * 2 * Cfg::LBO) >> 4);
+              const uint64_t b_lo = b_hi + (uint64_t)(Cfg::LO_OFF >> 4);
+              ptx::mma_tf32_ts_w(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+              ptx::mma_tf32_ts_w(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
+              ptx::mma_tf32_ts_w(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
             }
-            ptx::mma_commit(last_chunk ? &d_full[s] : &a_empty[s]);
+            ptx::mma_commit_w(last_chunk ? &d_full[s] : &a_empty[s]);
+            if (PROF) i_m += (unsigned long long)(clock64() - t0);
           }
-          ptx::mma_commit(&w_empty[ws]);
+          ptx::mma_commit_w(&w_empty[ws]);
           if (++ws == Cfg::STAGES) {
             ws = 0;
             wph ^= 1;
           }
         }
+      }
+      if (PROF && lane == 0) {
+        atomicAdd(a.prof + kFwdProfIssTotal, (unsigned long long)(clock64() - i_t0));
+        atomicAdd(a.prof + kFwdProfIssA, i_a);
+        atomicAdd(a.prof + kFwdProfIssW, i_w);
+        atomicAdd(a.prof + kFwdProfIssMma, i_m);
       }
     }
   } else {

@@ -519,9 +519,9 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     if (job >= 1) flush(job - 1);  // last dW job of this CTA
   } else if (warp == 8) {
     // ================================================================ MMA issuer
-    if (lane == 0) {
-      // fresh copy of the TMEM base: the shared prologue value may live in a spill slot
-      const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(tmem_base_slot);
+    // warp-uniform TMEM base; all 32 lanes run the schedule, mma/commit elect one lane
+    const uint32_t tm = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t*>(tmem_base_slot), 0);
+    {
       constexpr uint32_t idesc = ptx::idesc_tf32(128, H);
       constexpr uint32_t idesc_dw = ptx::idesc_tf32(128, 2 * H) | (1u << 15) | (1u << 16);  // A, B MN-major
       int ws = 0;
@@ -536,9 +536,9 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         for (int ks = 0; ks < H / 8; ++ks) {
           const uint64_t b_hi = d0 + (uint64_t)((ks * 2 * Cfg::LBO) >> 4);
           const uint64_t b_lo = b_hi + (uint64_t)(Cfg::LO_OFF >> 4);
-          ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (!first_zero || ks > 0) ? 1u : 0u);
-          ptx::mma_tf32_ts(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
-          ptx::mma_tf32_ts(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
+          ptx::mma_tf32_ts_w(slot + 2 * H, slot + 8 * ks, b_hi, idesc, (!first_zero || ks > 0) ? 1u : 0u);
+          ptx::mma_tf32_ts_w(slot + 2 * H, slot + 8 * ks, b_lo, idesc, 1u);
+          ptx::mma_tf32_ts_w(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
         }
       };
       unsigned long long pc_w = 0, pc_a = 0, pc_st = 0, pc_dw = 0;  // wait cycles (profiling only)
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         return ptx::smem_u32(wring + (size_t)ws * Cfg::CHUNK_FLOATS);
       };
       auto release_w = [&]() {
-        ptx::mma_commit(&w_empty[ws]);
+        ptx::mma_commit_w(&w_empty[ws]);
         if (++ws == Cfg::WSTAGES) {
           ws = 0;
           wph ^= 1;
@@ -582,15 +582,11 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ad = a0 + (uint64_t)((ks * 2 * Cfg::ST_SBO) >> 4);
             const uint64_t bd = ad + (uint64_t)(16384 >> 4);
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(t_dw),
-                "l"(ad), "l"(bd), "r"(idesc_dw), "r"((b > 0 || ks > 0) ? 1u : 0u)
-                : "memory");
+            ptx::mma_tf32_ss_w(t_dw, ad, bd, idesc_dw, (b > 0 || ks > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&st_empty[((gi / Cfg::NSTAGE) & 1) * Cfg::NSTAGE + buf]);
+          ptx::mma_commit_w(&st_empty[((gi / Cfg::NSTAGE) & 1) * Cfg::NSTAGE + buf]);
         }
-        ptx::mma_commit(dw_full);
+        ptx::mma_commit_w(dw_full);
         pdw ^= 1;
         if (PROF) pc_dwt += (unsigned long long)(clock64() - t_dw0);
       };
@@ -604,7 +600,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             pa[s] ^= 1;
             ptx::tc_fence_after();
             mma3(s, bb, c == 0);
-            ptx::mma_commit(c + 1 < nseg ? &a_empty[s] : &d_full[s]);
+            ptx::mma_commit_w(c + 1 < nseg ? &a_empty[s] : &d_full[s]);
           }
           release_w();
         }
@@ -615,7 +611,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             pa[s] ^= 1;
             ptx::tc_fence_after();
             mma3(s, bb, true);
-            ptx::mma_commit(&d_full[s]);
+            ptx::mma_commit_w(&d_full[s]);
           }
           release_w();
         }
@@ -630,7 +626,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             ptx::tc_fence_after();
             const long long t_m0 = PROF ? clock64() : 0;
             mma3(s, bb, step == 0);
-            ptx::mma_commit(&d_full[s]);
+            ptx::mma_commit_w(&d_full[s]);
             if (PROF) pc_mma += (unsigned long long)(clock64() - t_m0);
           }
           release_w();
@@ -644,13 +640,13 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             pa[s] ^= 1;
             ptx::tc_fence_after();
             mma3(s, bb, true);
-            ptx::mma_commit(&d_full[s]);
+            ptx::mma_commit_w(&d_full[s]);
           }
           release_w();
           dw_job();
         }
       }
-      if (PROF) {
+      if (PROF && lane == 0) {
         atomicAdd(a.prof + kProfTotal, (unsigned long long)(clock64() - t_start));
         atomicAdd(a.prof + kProfW, pc_w);
         atomicAdd(a.prof + kProfA, pc_a);
