@@ -81,7 +81,23 @@ class GraphDesc(C.Structure):
     ]
 
 
+def _preload_nccl() -> None:
+    """Bind libnccl.so.2 to the NCCL that PyTorch ships (nvidia-nccl wheel) when
+    present, so this library and torch.distributed share ONE NCCL in a process
+    regardless of import order (the system copy is older than torch's)."""
+    import sys
+    for base in sys.path:
+        cand = Path(base) / "nvidia" / "nccl" / "lib" / "libnccl.so.2"
+        if cand.exists():
+            try:
+                C.CDLL(str(cand), mode=C.RTLD_GLOBAL)
+            except OSError:
+                continue
+            return
+
+
 def _load() -> C.CDLL:
+    _preload_nccl()
     if not _LIB_PATH.exists():
         raise ImportError(
             f"{_LIB_PATH} is missing: build it with `python paper_2410_01657_b200/build.py` "
