@@ -33,6 +33,13 @@ def _f64(a: np.ndarray | None, shape=None):
     return a, a.ctypes.data_as(N.f64p)
 
 
+def _out(a: np.ndarray, shape) -> np.ndarray:
+    """Caller-provided output buffer: must be fp64, C-contiguous, right size."""
+    if a.dtype != np.float64 or not a.flags.c_contiguous or a.size != int(np.prod(shape)):
+        raise N.ShapeError(f"output buffer must be C-contiguous float64 of shape {shape}, got {a.dtype} {a.shape}")
+    return a.reshape(shape)
+
+
 class Engine:
     def __init__(self, device: int = 0, rank: int = 0, num_ranks: int = 1, uid: bytes | None = None):
         self._h = C.c_void_p()
@@ -73,27 +80,36 @@ class Engine:
         N.check(N.LIB.hgnn_params_upload(self._h, p, a.size))
 
     # ---- MP stack ----------------------------------------------------------
-    def nmp_forward(self, x0: np.ndarray, e0: np.ndarray, want_e: bool = False):
-        """Runs the M consistent NMP layers; returns x_M (rows x H) [and e_M]."""
+    def nmp_forward(self, x0: np.ndarray, e0: np.ndarray, want_e: bool = False, out=None):
+        """Runs the M consistent NMP layers; returns x_M (rows x H) [and e_M].
+        out: optional preallocated (x_M, e_M or None) fp64 C-contiguous arrays
+        (e.g. pinned host memory), written in place."""
         g, H = self.graph, self.cfg.hidden_dim
         x, xp = _f64(x0, (g.rows, H))
         e, ep = _f64(e0, (g.num_edges, H))
-        xo = np.empty((g.rows, H))
-        eo = np.empty((g.num_edges, H)) if want_e else None
+        if out is not None:
+            xo, eo = _out(out[0], (g.rows, H)), (_out(out[1], (g.num_edges, H)) if want_e else None)
+        else:
+            xo = np.empty((g.rows, H))
+            eo = np.empty((g.num_edges, H)) if want_e else None
         N.check(N.LIB.hgnn_mp_forward(self._h, xp, ep, xo.ctypes.data_as(N.f64p),
                                       eo.ctypes.data_as(N.f64p) if want_e else None))
         return (xo, eo) if want_e else xo
 
-    def nmp_backward(self, dx: np.ndarray, de: np.ndarray | None = None):
-        """Adjoint of the MP stack; returns (dx0, de0, mp_grads)."""
+    def nmp_backward(self, dx: np.ndarray, de: np.ndarray | None = None, out=None):
+        """Adjoint of the MP stack; returns (dx0, de0, mp_grads).
+        out: optional preallocated (dx0, de0, grads) fp64 arrays, written in place."""
         g, H = self.graph, self.cfg.hidden_dim
         d, dp = _f64(dx, (g.rows, H))
         e, epp = _f64(de, (g.num_edges, H))
-        dx0 = np.empty((g.rows, H))
-        de0 = np.empty((g.num_edges, H))
         n_par = self.cfg.num_mp_layers * (_mlp(3 * H, H, self.cfg.mlp_hidden_layers)
                                           + _mlp(2 * H, H, self.cfg.mlp_hidden_layers))
-        grads = np.empty(n_par)
+        if out is not None:
+            dx0, de0, grads = _out(out[0], (g.rows, H)), _out(out[1], (g.num_edges, H)), _out(out[2], (n_par,))
+        else:
+            dx0 = np.empty((g.rows, H))
+            de0 = np.empty((g.num_edges, H))
+            grads = np.empty(n_par)
         N.check(N.LIB.hgnn_mp_backward(self._h, dp, epp, dx0.ctypes.data_as(N.f64p), de0.ctypes.data_as(N.f64p),
                                        grads.ctypes.data_as(N.f64p)))
         return dx0, de0, grads
