@@ -95,18 +95,6 @@ __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool
   tc_gather<64, MODE>(f, row, valid, c, v);
 }
 
-// Scratch reload that the compiler may not merge with an earlier load of the
-// same address (keeps the 64 normed values out of registers between passes).
-__device__ __forceinline__ float4 ld_reload(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-  return v;
-}
-
-__device__ __forceinline__ void red_add4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
-
 // A <- [hi | lo] split of v, 16 columns at a time (low register pressure).
 __device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const float (&v)[64]) {
 #pragma unroll
@@ -296,6 +284,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     float* gpart0 = a.grad_partial + (int64_t)blockIdx.x * 2 * n_par;  // hh + hl, db
     float* gpart1 = gpart0 + n_par;                                    // lh
     const int trow = 32 * wq + lane;  // row inside the tile
+    const uint64_t keep = ptx::policy_evict_last();   // scratch, gradient partials
+    const uint64_t once = ptx::policy_evict_first();  // single-use streams
     uint32_t pe = 0, pd = 0;
     int64_t job = 0;                  // global dW job counter (all pairs)
 
@@ -336,8 +326,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       // (deterministic) and no load latency is exposed.
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        red_add4(gw + 4 * j, p0[4 * j], p0[4 * j + 1], p0[4 * j + 2], p0[4 * j + 3]);
-        red_add4(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3]);
+        ptx::red_add4_hint(gw + 4 * j, p0[4 * j], p0[4 * j + 1], p0[4 * j + 2], p0[4 * j + 3], keep);
+        ptx::red_add4_hint(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3], keep);
       }
       if (with_db && warp < 2) {  // bias gradient: fixed-order sum of the 8 warp partials
         const float* db = dbp + (jf % 3) * 8 * 64 + trow;
@@ -403,7 +393,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         const float inv_std = ln0_tree<H>(u);
         float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) st[q * 128] = make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+        for (int q = 0; q < 16; ++q)
+          ptx::st_hint(st + q * 128, make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]), keep);
         scr_inv[(l - 1) * 128 + trow] = inv_std;
 #pragma unroll
         for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
@@ -417,7 +408,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           const float4* de = reinterpret_cast<const float4*>(a.de_io + row * H);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float4 x1 = __ldg(da + q), x2 = de[q];
+            const float4 x1 = __ldg(da + q), x2 = ptx::ld_hint(de + q, once);  // read then rewritten in place: coherent path
             dh[4 * q] = fmaf(s, x1.x, x2.x);
             dh[4 * q + 1] = fmaf(s, x1.y, x2.y);
             dh[4 * q + 2] = fmaf(s, x1.z, x2.z);
@@ -456,7 +447,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float4 t4 = ld_reload(st + q * 128);
+          const float4 t4 = ptx::ld_hint(st + q * 128, keep);
           const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -476,7 +467,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float4 t4 = ld_reload(st + q * 128);
+          const float4 t4 = ptx::ld_hint(st + q * 128, keep);
           dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
           dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
           dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
@@ -510,7 +501,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           ptx::tmem_wait_ld();
           if (valid) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) o[cc / 4 + j] = make_float4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+            for (int j = 0; j < 4; ++j)
+              ptx::st_hint(o + cc / 4 + j, make_float4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]), once);
           }
         }
         if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays

@@ -53,3 +53,14 @@ ranked = sorted(per_line.items(), key=lambda kv: -sum(kv[1].values()))
 for ln, c in ranked[:top]:
     s = sum(c.values())
     print(f"{s / tot:6.3f} {ln:28s} {dict(c.most_common(3))}")
+if len(sys.argv) > 4:
+    print("--- top instructions")
+    inst = []
+    for r in data:
+        n = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+        off = int(r[ix["Address"]], 16) - base
+        ln, txt = lines_by_off.get(off, ("?", ""))
+        inst.append((n, off, ln, r[ix["Source"]].strip()[:70]))
+    inst.sort(reverse=True)
+    for n, off, ln, txt in inst[:int(sys.argv[4])]:
+        print(f"{n / tot:6.3f} {off:6x} {ln:24s} {txt}")
