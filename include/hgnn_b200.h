@@ -162,7 +162,9 @@ int hgnn_mp_step_device(hgnn_ctx* ctx);
 int hgnn_get_grads(hgnn_ctx* ctx, double* mp_grads);
 
 /* ---- options --------------------------------------------------------------- */
-/* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
+/* "mlp_forward_impl": 2 = tcgen05 tensor-core MLP forward, two epilogue threads
+ *                         per row (default; H = 64, else falls back to 1),
+ *                     1 = tcgen05, one epilogue thread per row (H in {32,64}),
  *                     0 = SIMT fp32 kernels.
  * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
  *                      0 = SIMT fp32 kernels. */
@@ -173,6 +175,14 @@ int hgnn_set_option(hgnn_ctx* ctx, const char* key, int64_t value);
  * row-major fp32; D 128x128). mode 0: A in TMEM + B K-major (forward / dX path),
  * 1: A and B MN-major in shared memory (dW path), 2: both K-major in shared memory. */
 int hgnn_selftest_mma(int mode, const float* A, const float* B, float* D);
+/* MMA issue-rate microbenchmark (debug aid): `blocks` CTAs each issue iters x 24
+ * kind::tf32 M=128 K=8 MMAs with N = n (A from TMEM if ts, else SMEM) into nd
+ * round-robin accumulators (nd * n <= 256 columns); cycles_out[b] = clock64
+ * cycles of CTA b from first issue to completion. */
+int hgnn_bench_mma(int iters, int n, int ts, int nd, int blocks, uint64_t* cycles_out);
+/* SFU / FMA throughput microbenchmark (debug aid): kind 0 ex2.approx, 1 fma,
+ * 2 rsqrt.approx; threads x 8 independent chains x iters operations per block. */
+int hgnn_bench_alu(int kind, int iters, int threads, int blocks, uint64_t* cycles_out);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* When enabled, every launch of the listed kernel classes is bracketed by CUDA
@@ -185,11 +195,11 @@ int hgnn_kernel_timing(hgnn_ctx* ctx, int enable);
 int hgnn_kernel_time(hgnn_ctx* ctx, int kernel_class, double* total_ms, int64_t* launches);
 /* Cycle counters of the tensor-core kernels (after hgnn_set_option(ctx,
  * "bwd_profile", 1); debugging aid, summed over CTAs):
- *   [0..8)   backward, edge MLP  (kProf* in mlp_tc_bwd.cuh)
- *   [8..16)  backward, node MLP
- *   [16..24) forward, edge MLP   (kFwdProf* in mlp_tc.cuh)
- *   [24..32) forward, node MLP */
-int hgnn_debug_profile(hgnn_ctx* ctx, uint64_t* out32);
+ *   [0..16)  backward, edge MLP  (kProf* in mlp_tc_bwd.cuh)
+ *   [16..32) backward, node MLP
+ *   [32..48) forward, edge MLP   (kFwdProf* in mlp_tc.cuh)
+ *   [48..64) forward, node MLP */
+int hgnn_debug_profile(hgnn_ctx* ctx, uint64_t* out64);
 /* Own-kernel launches issued since the last reset (for gpu_launches). */
 int64_t hgnn_launch_count(hgnn_ctx* ctx, int reset);
 /* Bytes handed to NCCL by this rank since the last reset (CommCounters analogue). */

@@ -131,6 +131,8 @@ def _load() -> C.CDLL:
         "hgnn_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
         "hgnn_selftest_mma": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
         "hgnn_debug_profile": (C.c_int, [vp, C.c_void_p]),
+        "hgnn_bench_mma": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+        "hgnn_bench_alu": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
         "hgnn_kernel_timing": (C.c_int, [vp, C.c_int]),
         "hgnn_kernel_time": (C.c_int, [vp, C.c_int, f64p, i64p]),
         "hgnn_launch_count": (C.c_int64, [vp, C.c_int]),
@@ -149,7 +151,7 @@ EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_grap
             "hgnn_ctx_create", "hgnn_ctx_destroy", "hgnn_ctx_stream", "hgnn_graph_upload", "hgnn_configure",
             "hgnn_params_upload", "hgnn_mp_forward", "hgnn_mp_backward", "hgnn_get_trace",
             "hgnn_synthetic_inputs", "hgnn_set_inputs", "hgnn_mp_step_device", "hgnn_get_grads",
-            "hgnn_set_option", "hgnn_selftest_mma", "hgnn_debug_profile", "hgnn_kernel_timing", "hgnn_kernel_time", "hgnn_launch_count", "hgnn_halo_bytes"]
+            "hgnn_set_option", "hgnn_selftest_mma", "hgnn_bench_mma", "hgnn_bench_alu", "hgnn_debug_profile", "hgnn_kernel_timing", "hgnn_kernel_time", "hgnn_launch_count", "hgnn_halo_bytes"]
 
 
 def check(status: int) -> None:

@@ -62,9 +62,10 @@ struct TcFwdArgs {
 // Optional instrumentation of the forward kernel (cycles summed over CTAs;
 // epilogue figures from warp 0 lane 0).
 enum { kFwdProfIssTotal = 0, kFwdProfIssA = 1, kFwdProfIssW = 2, kFwdProfIssMma = 3, kFwdProfEpiTotal = 4,
-       kFwdProfEpiD = 5, kFwdProfEpiAE = 6, kFwdProfEpiSig = 7 };
+       kFwdProfEpiD = 5, kFwdProfEpiAE = 6, kFwdProfEpiSig = 7, kFwdProfEpiLd = 8, kFwdProfEpiMath = 9,
+       kFwdProfEpiStA = 10, kFwdProfEpiGather = 11 /* whole input phase */, kFwdProfEpiOut = 12 };
 
-__device__ __forceinline__ float elu_fast(float z) { return z > 0.f ? z : __expf(z) - 1.0f; }
+__device__ __forceinline__ float elu_fast(float z) { return z > 0.f ? z : ptx::exp_fast(z) - 1.0f; }
 
 // Sum of H values with 8 independent partial sums (short dependency chains).
 template <int H>
@@ -90,7 +91,7 @@ __device__ __forceinline__ float ln0_tree(float (&v)[H]) {
     p[j % 8] = fmaf(d, d, p[j % 8]);
   }
   const float var = (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) * (1.0f / H);
-  const float inv_std = 1.0f / sqrtf(var + 1e-12f);
+  const float inv_std = ptx::rsqrt_fast(var + 1e-12f);
 #pragma unroll
   for (int j = 0; j < H; ++j) v[j] = (v[j] - mean) * inv_std;
   return inv_std;
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     const uint32_t t_alo = t_ahi + H;
     const uint32_t t_d = t_ahi + 2 * H;
     uint32_t pe = 0, pd = 0;
-    unsigned long long e_d = 0, e_ae = 0, e_sig = 0;
+    unsigned long long e_d = 0, e_ae = 0, e_sig = 0, e_ld = 0, e_math = 0, e_sta = 0, e_in = 0, e_out = 0;
     const long long e_t0 = PROF ? clock64() : 0;
     auto wait_d = [&]() {
       const long long t0 = PROF ? clock64() : 0;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       const int64_t row = (2 * pair + g) * 128 + 32 * wq + lane;
       const bool valid = row < a.n_rows;
       float h[H];
+      const long long t_in0 = PROF ? clock64() : 0;
       // input projection: nseg K-chunks streamed through A, next one prefetched
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
@@ -248,16 +250,32 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       }
       wait_d();
       tc_load_d<H>(t_d, sbias, h);
+      if (PROF) e_in += (unsigned long long)(clock64() - t_in0);
       // residual blocks
       for (int l = 1; l <= a.k; ++l) {
+        long long t0 = PROF ? clock64() : 0;
         tc_store_a<H>(t_ahi, t_alo, h);
+        if (PROF) {
+          const long long t1 = clock64();
+          e_sta += (unsigned long long)(t1 - t0);
+        }
         signal_a();
         wait_d();
+        if (PROF) t0 = clock64();
         float u[H];
         tc_load_d<H>(t_d, sbias + l * H, u);
+        if (PROF) {
+          const long long t1 = clock64();
+          e_ld += (unsigned long long)(t1 - t0);
+          t0 = t1;
+        }
         ln0_tree<H>(u);
 #pragma unroll
         for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
+        if (PROF) {
+          __syncwarp();
+          e_math += (unsigned long long)(clock64() - t0);
+        }
       }
       // output projection; the next tile's first segment is gathered meanwhile
       tc_store_a<H>(t_ahi, t_alo, h);
@@ -268,6 +286,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         tc_gather<H, MODE>(a, nrow, nrow < a.n_rows, 0, v);
       }
       wait_d();
+      const long long t_out0 = PROF ? clock64() : 0;
       {  // stream y = D + b straight to global, 32 columns at a time
         const float* bo = sbias + (a.k + 1) * H;
         float4* o = reinterpret_cast<float4*>(a.out + row * H);
@@ -284,12 +303,18 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
           }
         }
       }
+      if (PROF) e_out += (unsigned long long)(clock64() - t_out0);
     }
     if (PROF && warp == 0 && lane == 0) {
       atomicAdd(a.prof + kFwdProfEpiTotal, (unsigned long long)(clock64() - e_t0));
       atomicAdd(a.prof + kFwdProfEpiD, e_d);
       atomicAdd(a.prof + kFwdProfEpiAE, e_ae);
       atomicAdd(a.prof + kFwdProfEpiSig, e_sig);
+      atomicAdd(a.prof + kFwdProfEpiLd, e_ld);
+      atomicAdd(a.prof + kFwdProfEpiMath, e_math);
+      atomicAdd(a.prof + kFwdProfEpiStA, e_sta);
+      atomicAdd(a.prof + kFwdProfEpiGather, e_in);
+      atomicAdd(a.prof + kFwdProfEpiOut, e_out);
     }
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer

@@ -82,7 +82,8 @@ struct TcBwdArgs {
 
 // Optional instrumentation of the MMA issuer (cycles, summed over CTAs).
 enum { kProfTotal = 0, kProfW = 1, kProfA = 2, kProfSt = 3, kProfDwE = 4, kProfFwd = 5, kProfDw = 6, kProfMma = 7,
-       kProfCount = 8 };
+       kProfEpiTotal = 8, kProfEpiRecompute = 9, kProfEpiFlush = 10, kProfEpiStage = 11, kProfEpiDb = 12,
+       kProfEpiWaitDx = 13, kProfEpiLnBwd = 14, kProfEpiInput = 15, kProfCount = 16 };
 
 template <int MODE>
 __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64]) {
@@ -288,11 +289,14 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     const uint64_t once = ptx::policy_evict_first();  // single-use streams
     uint32_t pe = 0, pd = 0;
     int64_t job = 0;                  // global dW job counter (all pairs)
+    unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // epilogue cycle counters (PROF)
+    const long long pf_t0 = PROF ? clock64() : 0;
 
     // Drain the dW accumulator of global job jf: this warp reads its TMEM lane
     // quarter, column half g. Lanes < 64 hold (h_hi row i) x [d_hi | d_lo]:
     // hh + hl; lanes >= 64 hold (h_lo row i - 64) x d_hi: lh.
     auto flush = [&](int64_t jf) {
+      const long long tf0 = PROF ? clock64() : 0;
       const int jj = (int)(jf % n_dw);
       const int lin = jj <= K ? K + 1 - jj : 0;
       const int rowbase = jj <= K ? 0 : (jj - K - 1) * H;
@@ -337,11 +341,13 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(s)
                      : "memory");
       }
+      if (PROF) pf[2] += (unsigned long long)(clock64() - tf0);
     };
     // The previous job's dW must be drained first: this job's staging ring
     // slots are only released by dW MMAs that accumulate onto it.
     auto stage_chunk = [&](const float (&hin)[H], const float (&d)[H]) {
       if (job >= 1) flush(job - 1);
+      const long long ts0 = PROF ? clock64() : 0;
       const int64_t gi = job * 8 + warp;  // staging chunk counter
       stage_acquire(st_empty, gi);
       uint8_t* sb = stage + (size_t)(gi % Cfg::NSTAGE) * Cfg::STAGE_BYTES;
@@ -350,23 +356,29 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&st_full[gi % Cfg::NSTAGE]);
+      if (PROF) pf[3] += (unsigned long long)(clock64() - ts0);
     };
     auto write_db = [&](const float (&d)[H]) {
+      const long long t0 = PROF ? clock64() : 0;
       const float2 cs = warp_colsum64(d);
       float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
       dst[0] = cs.x;
       dst[1] = cs.y;
+      if (PROF) pf[4] += (unsigned long long)(clock64() - t0);
     };
     auto wait_dx = [&]() {
+      const long long t0 = PROF ? clock64() : 0;
       ptx::mbar_wait(&d_full[g], pd);
       pd ^= 1;
       ptx::tc_fence_after();
+      if (PROF) pf[5] += (unsigned long long)(clock64() - t0);
     };
 
     for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
       const int64_t row = (2 * pair + g) * 128 + trow;
       const bool valid = row < a.n_rows;
       float h[H];
+      const long long tr0 = PROF ? clock64() : 0;
       // ---------------------------------------------- forward recompute
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
@@ -399,6 +411,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
 #pragma unroll
         for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
       }
+      if (PROF) pf[1] += (unsigned long long)(clock64() - tr0);
       // ---------------------------------------------- backward
       float dh[H];
       if (valid) {
@@ -441,6 +454,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       for (int l = K; l >= 1; --l) {
         const float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
         const float inv_std = scr_inv[(l - 1) * 128 + trow];
+        const long long tl0 = PROF ? clock64() : 0;
         bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
         float p1[8], p2[8];
 #pragma unroll
@@ -453,7 +467,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * q + u;
             const float t = tv[u];
-            const float ex = __expf(t);
+            const float ex = ptx::exp_fast(t);
             const float elu = t > 0.f ? t : ex - 1.0f;
             const float dd = dh[j] * (t > 0.f ? 1.0f : ex);  // elu', kernels.cpp:68-71
             h[j] -= elu;                                     // h_{l-1}
@@ -473,6 +487,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
           dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
         }
+        if (PROF) pf[6] += (unsigned long long)(clock64() - tl0);
         bwd_store_a(t_ahi, t_alo, dh);
         tc_signal(&a_full[g]);
         write_db(dh);
@@ -481,6 +496,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         ++job;
         bwd_load_d(t_d, nullptr, dh);  // d_prev = d_u W^T + d_h
       }
+      const long long ti0 = PROF ? clock64() : 0;
       // input projection (nn.cpp:277-281): per segment c, dW0[seg c] and d_in[seg c]
       bwd_store_a(t_ahi, t_alo, dh);
       tc_signal(&a_full[g]);
@@ -507,8 +523,14 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         }
         if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays
       }
+      if (PROF) pf[7] += (unsigned long long)(clock64() - ti0);
     }
     if (job >= 1) flush(job - 1);  // last dW job of this CTA
+    if (PROF && warp == 0 && lane == 0) {
+      pf[0] = (unsigned long long)(clock64() - pf_t0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) atomicAdd(a.prof + kProfEpiTotal + i, pf[i]);
+    }
   } else if (warp == 8) {
     // ================================================================ MMA issuer
     // warp-uniform TMEM base; all 32 lanes run the schedule, mma/commit elect one lane

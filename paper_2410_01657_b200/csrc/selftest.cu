@@ -141,3 +141,134 @@ extern "C" int hgnn_selftest_mma(int mode, const float* A, const float* B, float
     if (e != cudaSuccess) fail(HGNN_ERR_CUDA, cudaGetErrorString(e));
   });
 }
+
+// ---- MMA issue-rate microbenchmark (debug aid) ------------------------------
+// One CTA per SM issues `iters` x 24 tcgen05.mma (kind::tf32, M = 128, K = 8)
+// back to back from an elected lane of warp 0 with warp-uniform operands,
+// N = n, A from TMEM (ts) or shared memory, B from shared memory, into nd
+// round-robin accumulators. Operands are uninitialised (timing only).
+// cycles[blockIdx] = clock64 span from first issue to commit arrival.
+namespace {
+template <int N, bool TS, int ND>
+__global__ void __launch_bounds__(128) mma_rate_kernel(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<512>(&tslot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, tslot, 0);
+  if (warp == 0) {
+    constexpr uint32_t idesc = ptx::idesc_tf32(128, N);
+    const uint32_t base = ptx::smem_u32(sm);
+    const uint64_t bd = ptx::smem_desc(base, (uint32_t)(N / 8) * 128, 128);
+    const uint64_t ad = ptx::smem_desc(base + 65536, 16 * 128, 128);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int j = 0; j < 24; ++j) {
+        const uint32_t dcol = tmem + 256 + (uint32_t)((j % ND) * (256 / ND));
+        if (TS) ptx::mma_tf32_ts_w(dcol, tmem + 8 * (j % 16), bd + (uint64_t)(j % 8) * 16, idesc, 1u);
+        else ptx::mma_tf32_ss_w(dcol, ad + (uint64_t)(j % 8) * 16, bd + (uint64_t)(j % 8) * 16, idesc, 1u);
+      }
+    }
+    ptx::mma_commit_w(&bar);
+    ptx::mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int N, bool TS, int ND>
+void run_rate(int iters, int blocks, unsigned long long* d) {
+  cudaFuncSetAttribute(mma_rate_kernel<N, TS, ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  mma_rate_kernel<N, TS, ND><<<blocks, 128, 160 * 1024>>>(iters, d);
+}
+}  // namespace
+
+extern "C" int hgnn_bench_mma(int iters, int n, int ts, int nd, int blocks, uint64_t* cycles_out) {
+  return guarded([&] {
+    unsigned long long* d;
+    if (cudaMalloc(&d, sizeof(unsigned long long) * (size_t)blocks)) fail(HGNN_ERR_CUDA, "bench alloc");
+    const int key = n * 100 + (ts ? 10 : 0) + nd;
+    switch (key) {
+      case 6411: run_rate<64, true, 1>(iters, blocks, d); break;
+      case 6412: run_rate<64, true, 2>(iters, blocks, d); break;
+      case 12811: run_rate<128, true, 1>(iters, blocks, d); break;
+      case 12812: run_rate<128, true, 2>(iters, blocks, d); break;
+      case 25611: run_rate<256, true, 1>(iters, blocks, d); break;
+      case 6401: run_rate<64, false, 1>(iters, blocks, d); break;
+      case 12801: run_rate<128, false, 1>(iters, blocks, d); break;
+      case 25601: run_rate<256, false, 1>(iters, blocks, d); break;
+      default: fail(HGNN_ERR_CONFIG, "hgnn_bench_mma: unsupported (n, ts, nd)");
+    }
+    const cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(cycles_out, d, sizeof(unsigned long long) * (size_t)blocks, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) fail(HGNN_ERR_CUDA, cudaGetErrorString(e));
+  });
+}
+
+// ---- SFU / FMA throughput microbenchmark (debug aid) -------------------------
+// Each of `threads` threads runs 8 independent chains of `iters` operations:
+// kind 0: ex2.approx.ftz.f32, kind 1: fma.rn.f32, kind 2: rsqrt.approx.
+// cycles[b] = clock64 span of thread 0 of block b; sink keeps the results live.
+namespace {
+__global__ void alu_rate_kernel(int kind, int iters, unsigned long long* cycles, float* sink) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  const long long t0 = clock64();
+  if (kind == 0) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
+    }
+  } else if (kind == 1) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32 %0, %0, 0f3F7FFFFF, 0f3A83126F;" : "+f"(v[i]));
+    }
+  } else {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += v[i];
+  if (s == 12345.f) sink[threadIdx.x] = s;
+}
+}  // namespace
+
+extern "C" int hgnn_bench_alu(int kind, int iters, int threads, int blocks, uint64_t* cycles_out) {
+  return guarded([&] {
+    unsigned long long* d;
+    float* sink;
+    if (cudaMalloc(&d, sizeof(unsigned long long) * (size_t)blocks) || cudaMalloc(&sink, 4096 * 4))
+      fail(HGNN_ERR_CUDA, "bench alloc");
+    alu_rate_kernel<<<blocks, threads>>>(kind, iters, d, sink);
+    const cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(cycles_out, d, sizeof(unsigned long long) * (size_t)blocks, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(sink);
+    if (e != cudaSuccess) fail(HGNN_ERR_CUDA, cudaGetErrorString(e));
+  });
+}

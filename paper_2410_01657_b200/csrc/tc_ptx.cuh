@@ -205,6 +205,21 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 // fp32 -> tf32 by truncation (one LOP3): hi = x with the 13 low mantissa bits
 // cleared; x - hi is exact in fp32 and |x - hi| < 2^-10 |x|, so the 3xTF32
 // split hi*hi + hi*lo + lo*hi keeps ~2^-20 relative accuracy per product.
+// ---- fast transcendental helpers (single SFU op, no denormal fix-up code) --
+// exp(x) = 2^(x log2 e) with ex2.approx.ftz (2 ulp; results below 2^-126 flush
+// to 0, which only affects ELU at z < -87 where the value is -1 either way).
+__device__ __forceinline__ float exp_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
+}
+// 1/sqrt(x), rsqrt.approx.ftz (max rel. error 2^-22.9)
+__device__ __forceinline__ float rsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ---- L2 residency hints ------------------------------------------------------
 // Per-CTA scratch and gradient partials are re-touched within microseconds and
 // must stay in L2 (evict_last); single-use streams should not displace them

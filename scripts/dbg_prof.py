@@ -12,16 +12,20 @@ for E in (8,):
     eng.kernel_timing(True)
     eng.step_device()
     kt = eng.kernel_times()
-    out = np.zeros(32, np.uint64)
+    out = np.zeros(64, np.uint64)
     N.check(N.LIB.hgnn_debug_profile(eng._h, out.ctypes.data))
     names = ["total", "w_full", "a_full", "st_full", "dw_empty", "fwd_phase", "dw_job", "mma3_bwd"]
     print("E", E, "edges", g.num_edges, {kk: round(v[0], 3) for kk, v in kt.items()})
-    for w, base in (("edge", 0), ("node", 8)):
+    for w, base in (("edge", 0), ("node", 16)):
         tot = out[base] or 1
         print(w, {names[i]: f"{out[base+i]/tot:.3f}" for i in range(8)}, "total Mcyc/CTA", out[base] / 148 / 1e6)
-    fn = ["iss_total", "iss_wait_a", "iss_wait_w", "iss_mma", "epi_total", "epi_wait_d", "epi_wait_aempty", "epi_signal"]
-    for w, base in (("fwd edge", 16), ("fwd node", 24)):
-        print(w, {fn[i]: f"{out[base+i]/max(out[base + (0 if i < 4 else 4)],1):.3f}" for i in range(8)},
+    en = ["epi_total", "recompute", "flush", "stage", "write_db", "wait_dx", "ln_bwd", "input_phase"]
+    for w, base in (("edge", 0), ("node", 16)):
+        tot = out[base + 8] or 1
+        print(w, "epilogue", {en[i]: f"{out[base+8+i]/tot:.3f}" for i in range(8)}, "Mcyc/CTA", out[base + 8] / 148 / 1e6)
+    fn = ["iss_total", "iss_wait_a", "iss_wait_w", "iss_mma", "epi_total", "epi_wait_d", "epi_wait_aempty", "epi_signal", "epi_ld", "epi_math", "epi_store_a"]
+    for w, base in (("fwd edge", 32), ("fwd node", 48)):
+        print(w, {fn[i]: f"{out[base+i]/max(out[base + (0 if i < 4 else 4)],1):.3f}" for i in range(11)},
               "iss Mcyc/CTA", out[base] / 148 / 1e6, "epi Mcyc/CTA", out[base + 4] / 148 / 1e6)
     eng.set_option("bwd_profile", 0)
     for impl in (0, 1):
