@@ -162,9 +162,7 @@ int hgnn_mp_step_device(hgnn_ctx* ctx);
 int hgnn_get_grads(hgnn_ctx* ctx, double* mp_grads);
 
 /* ---- options --------------------------------------------------------------- */
-/* "mlp_forward_impl": 2 = tcgen05 tensor-core MLP forward, two epilogue threads
- *                         per row (default; H = 64, else falls back to 1),
- *                     1 = tcgen05, one epilogue thread per row (H in {32,64}),
+/* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
  *                     0 = SIMT fp32 kernels.
  * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
  *                      0 = SIMT fp32 kernels. */

@@ -30,7 +30,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-Xcompiler", "-Wall"]
 
 SOURCES = ["engine.cu", "selftest.cu", "host_graph.cpp", "host_params.cpp"]
-HEADERS = ["common.hpp", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc2.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh"]
+HEADERS = ["common.hpp", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh"]
 
 
 def _newer(src: list[Path], out: Path) -> bool:

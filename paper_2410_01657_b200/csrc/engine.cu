@@ -22,7 +22,6 @@
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
 #include "mlp_tc_bwd.cuh"
-#include "mlp_tc2.cuh"
 
 using namespace hgnn_b200;
 
@@ -102,7 +101,7 @@ struct hgnn_ctx {
   DevBuf<float> chunks;                 // tcgen05 B operands, [W_hi | W_lo]^T chunks per MLP
   std::vector<int64_t> chunk_off;       // per (layer, edge/node)
   DevBuf<double> grads;
-  int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64}), 2 = tcgen05 column-split (H = 64)
+  int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
   int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
   DevBuf<float> bchunks;                // backward chunk sequence per MLP
   std::vector<int64_t> bchunk_off;
@@ -501,7 +500,7 @@ MlpParamsDev layer_params(hgnn_ctx* c, int64_t m, bool edge) {
   return p;
 }
 
-bool use_tc(const hgnn_ctx* c) { return c->fwd_impl >= 1 && tc_eligible(c); }
+bool use_tc(const hgnn_ctx* c) { return c->fwd_impl == 1 && tc_eligible(c); }
 
 template <int H, int MODE>
 void launch_tc_typed(hgnn_ctx* c, const TcFwdArgs& args) {
@@ -516,21 +515,6 @@ void launch_tc_typed(hgnn_ctx* c, const TcFwdArgs& args) {
   const int64_t pairs = ((args.n_rows + 127) / 128 + 1) / 2;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
   k<<<grid, Cfg::THREADS, Cfg::SMEM, c->stream>>>(args);
-  check_launch(c);
-}
-
-template <int MODE>
-void launch_tc2_typed(hgnn_ctx* c, const TcFwdArgs& args) {
-  const bool prof = args.prof != nullptr;
-  auto k = prof ? mlp_tc_forward2_kernel<MODE, true> : mlp_tc_forward2_kernel<MODE, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[prof]) {
-    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tc2Cfg::SMEM));
-    attr[prof] = true;
-  }
-  const int64_t pairs = ((args.n_rows + 127) / 128 + 1) / 2;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
-  k<<<grid, Tc2Cfg::THREADS, Tc2Cfg::SMEM, c->stream>>>(args);
   check_launch(c);
 }
 
@@ -550,10 +534,7 @@ void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const f
   args.params = layer_params(c, m, edge).p;
   args.k = (int)c->K;
   args.prof = c->prof_on ? c->prof.p + 2 * kProfCount + (edge ? 0 : kProfCount) : nullptr;
-  if (c->H == 64 && c->fwd_impl == 2) {
-    if (edge) launch_tc2_typed<kEdgeInput>(c, args);
-    else launch_tc2_typed<kNodeInput>(c, args);
-  } else if (c->H == 64) {
+  if (c->H == 64) {
     if (edge) launch_tc_typed<64, kEdgeInput>(c, args);
     else launch_tc_typed<64, kNodeInput>(c, args);
   } else {
@@ -1155,8 +1136,7 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
     bind(c);
     const std::string k = key ? key : "";
     if (k == "mlp_forward_impl") {
-      if (value < 0 || value > 2)
-        fail(HGNN_ERR_CONFIG, "mlp_forward_impl: 0 (simt), 1 (tcgen05), 2 (tcgen05 column-split, H = 64)");
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_forward_impl: 0 (simt) or 1 (tcgen05)");
       c->fwd_impl = (int)value;
     } else if (k == "bwd_profile") {
       c->prof.alloc(4 * kProfCount);

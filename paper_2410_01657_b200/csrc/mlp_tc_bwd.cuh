@@ -154,20 +154,35 @@ __device__ __forceinline__ uint32_t st_off(int mn4, int row) {
 }
 
 // Writes [v_hi | v_lo] (128 MN entries) of this lane's row into a staging operand.
+// Bank-conflict-free: a 16-byte store is served per quarter warp (8 lanes);
+// lanes r and r + 4 share r % 4, i.e. the same swizzled 32-byte granule, so
+// lanes with bit 2 of the row set store the two 16-byte halves of each
+// granule in the opposite order (chunk pair (2p, 2p+1) swapped).
 __device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&v)[64]) {
+  const bool sw = (row >> 2) & 1;
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    float4 hi, lo;
-    hi.x = ptx::tf32_trunc(v[4 * q]);
-    hi.y = ptx::tf32_trunc(v[4 * q + 1]);
-    hi.z = ptx::tf32_trunc(v[4 * q + 2]);
-    hi.w = ptx::tf32_trunc(v[4 * q + 3]);
-    lo.x = v[4 * q] - hi.x;
-    lo.y = v[4 * q + 1] - hi.y;
-    lo.z = v[4 * q + 2] - hi.z;
-    lo.w = v[4 * q + 3] - hi.w;
-    *reinterpret_cast<float4*>(base + st_off(q, row)) = hi;
-    *reinterpret_cast<float4*>(base + st_off(16 + q, row)) = lo;
+  for (int p = 0; p < 8; ++p) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int qa = 2 * p + k, qb = 2 * p + (k ^ 1);
+      float4 x;
+      x.x = sw ? v[4 * qb] : v[4 * qa];
+      x.y = sw ? v[4 * qb + 1] : v[4 * qa + 1];
+      x.z = sw ? v[4 * qb + 2] : v[4 * qa + 2];
+      x.w = sw ? v[4 * qb + 3] : v[4 * qa + 3];
+      const int q = sw ? qb : qa;
+      float4 hi, lo;
+      hi.x = ptx::tf32_trunc(x.x);
+      hi.y = ptx::tf32_trunc(x.y);
+      hi.z = ptx::tf32_trunc(x.z);
+      hi.w = ptx::tf32_trunc(x.w);
+      lo.x = x.x - hi.x;
+      lo.y = x.y - hi.y;
+      lo.z = x.z - hi.z;
+      lo.w = x.w - hi.w;
+      *reinterpret_cast<float4*>(base + st_off(q, row)) = hi;
+      *reinterpret_cast<float4*>(base + st_off(16 + q, row)) = lo;
+    }
   }
 }
 

@@ -155,22 +155,21 @@ def test_backward_before_forward_is_uninitialized(gpus):
 
 @pytest.mark.parametrize("H,k", [(32, 5), (64, 5), (64, 0), (32, 2)])
 def test_tensor_core_forward_matches_simt_and_oracle(engine, H, k):
-    """tcgen05 3xTF32 MLP forward (one and two epilogue threads per row) vs the
-    SIMT fp32 kernels vs the fp64 oracle."""
+    """tcgen05 3xTF32 MLP forward vs the SIMT fp32 kernels vs the fp64 oracle."""
     M = 2
     cfg = GnnConfig("tc", H, M, k, mode="na2a")
     g = build_rank_graph(3, 3, 1, 0, "verify")
     mp = mp_params(cfg, init_params(cfg, 11))
     x0, e0, dx, de = random_inputs(g, H, 5)
     outs = {}
-    impls = (0, 1, 2) if H == 64 else (0, 1)
+    impls = (0, 1)
     for impl in impls:
         engine.upload_graph(g)
         engine.configure(cfg)
         engine.upload_params(mp)
         engine.set_option("mlp_forward_impl", impl)
         outs[impl] = engine.nmp_forward(x0, e0, want_e=True)
-    engine.set_option("mlp_forward_impl", 2)
+    engine.set_option("mlp_forward_impl", 1)
     ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
     for impl in impls:
         assert rel(outs[impl][0], ref["x_out"][0][M - 1]) < FWD_TOL, impl
