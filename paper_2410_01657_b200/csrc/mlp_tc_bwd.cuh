@@ -8,24 +8,26 @@
 // Per CTA (persistent, one per SM), two 128-row tile slots ping-pong as in
 // the forward kernel. TMEM (512 columns):
 //   slot s: [A_hi 64 | A_lo 64 | D 64]  (s = 0, 1)      cols [192 s, 192 s + 192)
-//   dW accumulator 128 x 128                             cols [384, 512)
-// The dW product is one stacked MMA per K-step:
-//   [h_hi^T ; h_lo^T] (128 x 8) x [d_hi | d_lo] (8 x 128)
-// whose quadrants hh + hl + lh are the 3xTF32 gradient (ll is dropped). Both
-// operands are staged per warp (32 rows) in shared memory as MN-major
-// SWIZZLE_128B_BASE32B tiles (the layout tf32 MN-major operands require),
-// through a ring of NSTAGE buffers consumed by the MMA issuer in a fixed warp
-// order (deterministic accumulation). The epilogue warps drain the
-// accumulator of job j before staging job j + 1 (whose ring slots are only
-// recycled by MMAs onto that accumulator): each warp owns its TMEM lane quarter and one column
-// half, adding hh + hl into a per-CTA fp32 partial and lh into a second one
-// (one owning thread per element: deterministic); bias gradients come from
+//   dW accumulators 2 x (128 x 64), by job parity        cols [384, 448), [448, 512)
+// Per 8-row K-step the dW product is two SS MMAs into one accumulator:
+//   [h_hi^T ; h_lo^T] (128 x 8) x d_hi (8 x 64)  and  ... x d_lo (8 x 64),
+// so lanes 0-63 collect hh + hl and lanes 64-127 lh + ll (the tiny ll term is
+// kept: free and slightly more accurate). Both operands are staged per warp
+// (32 rows) in shared memory as MN-major SWIZZLE_128B_BASE32B tiles (the layout
+// tf32 MN-major operands require), through a ring of NSTAGE buffers consumed
+// in a fixed warp order (deterministic accumulation) by a dW issuer warp that
+// runs separately from the dX issuer. With two accumulators, job j drains
+// while job j + 1 accumulates: the epilogue warps drain job j - 2 before
+// staging job j, each warp its TMEM lane quarter and one column half, adding
+// hh + hl into a per-CTA fp32 partial and lh + ll into a second one (one
+// owning thread per element: deterministic); bias gradients come from
 // fixed-order per-warp column sums.
 // Forward-recompute intermediates of the reverse pass (normed t_j, inv_std_j)
 // go to a per-CTA global scratch; the residual stream is rebuilt backwards as
 // h_{j-1} = h_j - ELU(t_j). The residual term of d_prev = d_u W^T + d_h is
 // folded into the MMA by pre-loading D with d_h.
-// Warp roles: 0-7 epilogue (slot = warp / 4), 8 MMA issuer, 9 weight loader, 10-11 idle.
+// Warp roles: 0-7 epilogue (slot = warp / 4), 8 dX issuer, 9 dW issuer,
+// 10 weight loader, 11 idle.
 #pragma once
 
 #include "mlp_tc.cuh"
@@ -47,12 +49,12 @@ struct TcBwdCfg {
   static constexpr uint32_t ST_LBO = 512;              // MN-atom stride (32 tf32 of MN)
   static constexpr uint32_t ST_SBO = 2048;             // K-atom stride (4 rows): 128 MN = 4 atoms
   static constexpr int SLOT_COLS = 3 * H;
-  static constexpr int DW_COL = 2 * SLOT_COLS;         // 384
+  static constexpr int DW_COL = 2 * SLOT_COLS;         // 384: two 64-column dW accumulators (job parity)
   static constexpr int THREADS = 384;  // 2 epilogue warpgroups + 1 control warpgroup
   static constexpr size_t OFF_STAGE = (size_t)WSTAGES * CHUNK_BYTES;
   static constexpr size_t OFF_BARS = OFF_STAGE + (size_t)NSTAGE * STAGE_BYTES;
-  static constexpr size_t OFF_DBP = OFF_BARS + 256;               // db partials [3][8][64]
-  static constexpr size_t OFF_BIAS = OFF_DBP + 3 * 8 * 64 * 4;    // biases (k+2) x 64
+  static constexpr size_t OFF_DBP = OFF_BARS + 256;               // db partials [4][8][64]
+  static constexpr size_t OFF_BIAS = OFF_DBP + 4 * 8 * 64 * 4;    // biases (k+2) x 64
   static constexpr size_t SMEM = OFF_BIAS + 18 * 64 * 4 + 1024;
 };
 
@@ -238,9 +240,9 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   uint64_t* st_full = d_full + 2;                 // [NSTAGE]
   uint64_t* st_empty = st_full + Cfg::NSTAGE;     // [2][NSTAGE]: split by use parity so a producer
                                                   // running a whole job ahead cannot alias a phase
-  uint64_t* dw_full = st_empty + 2 * Cfg::NSTAGE; // [1]
-  uint64_t* dw_empty = dw_full + 1;               // [1], count 8 (epilogue warps)
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(dw_empty + 1);
+  uint64_t* dw_full = st_empty + 2 * Cfg::NSTAGE; // [2] per accumulator
+  uint64_t* dw_empty = dw_full + 2;               // [2], count 8 (epilogue warps)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(dw_empty + 2);
   float* dbp = reinterpret_cast<float*>(smem + Cfg::OFF_DBP);
   float* sbias = reinterpret_cast<float*>(smem + Cfg::OFF_BIAS);
 
@@ -268,8 +270,10 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       ptx::mbar_init(&st_empty[s], 1);
       ptx::mbar_init(&st_empty[Cfg::NSTAGE + s], 1);
     }
-    ptx::mbar_init(dw_full, 1);
-    ptx::mbar_init(dw_empty, 8);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&dw_full[s], 1);
+      ptx::mbar_init(&dw_empty[s], 8);
+    }
     ptx::fence_mbarrier_init();
   }
   for (int i = threadIdx.x; i < (K + 2) * H; i += blockDim.x)
@@ -307,39 +311,36 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // epilogue cycle counters (PROF)
     const long long pf_t0 = PROF ? clock64() : 0;
 
-    // Drain the dW accumulator of global job jf: this warp reads its TMEM lane
-    // quarter, column half g. Lanes < 64 hold (h_hi row i) x [d_hi | d_lo]:
-    // hh + hl; lanes >= 64 hold (h_lo row i - 64) x d_hi: lh.
+    // Drain dW job jf from accumulator jf & 1 (two 64-column accumulators in
+    // TMEM, so job jf + 1 accumulates while jf drains): this warp reads its
+    // lane quarter, output columns [32 g, 32 g + 32). Lanes < 64 hold
+    // (h_hi row i) x (d_hi + d_lo) = hh + hl; lanes >= 64 hold
+    // (h_lo row i - 64) x (d_hi + d_lo) = lh + ll.
     auto flush = [&](int64_t jf) {
       const long long tf0 = PROF ? clock64() : 0;
       const int jj = (int)(jf % n_dw);
       const int lin = jj <= K ? K + 1 - jj : 0;
       const int rowbase = jj <= K ? 0 : (jj - K - 1) * H;
       const bool with_db = jj <= K + 1;
-      ptx::mbar_wait(dw_full, (uint32_t)(jf & 1));
+      const int acc = (int)(jf & 1);
+      ptx::mbar_wait(&dw_full[acc], (uint32_t)((jf >> 1) & 1));
       ptx::tc_fence_after();
       const int c0 = 32 * g;
       float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow) * H + c0
                          : gpart1 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow - 64) * H + c0;
       float p0[16], p1[16];
-      ptx::tmem_ld16(t_dw + c0, p0);
-      ptx::tmem_ld16(t_dw + c0 + 16, p1);
-      if (wq < 2) {
-        float q0[16], q1[16];
-        ptx::tmem_ld16(t_dw + 64 + c0, q0);
-        ptx::tmem_ld16(t_dw + 64 + c0 + 16, q1);
-        ptx::tmem_wait_ld();
+      ptx::tmem_ld16(t_dw + 64 * acc + c0, p0);
+      ptx::tmem_ld16(t_dw + 64 * acc + c0 + 16, p1);
+      float dbs = 0.f;
+      if (with_db && warp < 2) {  // bias gradient: fixed-order sum of the 8 warp partials
+        const float* db = dbp + (jf % 4) * 8 * 64 + trow;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          p0[j] += q0[j];
-          p1[j] += q1[j];
-        }
-      } else {
-        ptx::tmem_wait_ld();
+        for (int w = 0; w < 8; ++w) dbs += db[w * 64];
       }
+      ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(dw_empty);  // this warp's part of the accumulator is read
+      if (lane == 0) ptx::mbar_arrive(&dw_empty[acc]);  // this warp's part is read (and its db partials)
       // Fire-and-forget vector reductions into this CTA's partial: every
       // element has a single owning thread, so the adds land in program order
       // (deterministic) and no load latency is exposed.
@@ -348,20 +349,15 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         ptx::red_add4_hint(gw + 4 * j, p0[4 * j], p0[4 * j + 1], p0[4 * j + 2], p0[4 * j + 3], keep);
         ptx::red_add4_hint(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3], keep);
       }
-      if (with_db && warp < 2) {  // bias gradient: fixed-order sum of the 8 warp partials
-        const float* db = dbp + (jf % 3) * 8 * 64 + trow;
-        float s = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s += db[w * 64];
-        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(s)
+      if (with_db && warp < 2)
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(dbs)
                      : "memory");
-      }
       if (PROF) pf[2] += (unsigned long long)(clock64() - tf0);
     };
-    // The previous job's dW must be drained first: this job's staging ring
-    // slots are only released by dW MMAs that accumulate onto it.
+    // Job j - 2 shares this job's accumulator and must be drained before the
+    // dW MMAs of job j (which release this job's staging ring slots) can run.
     auto stage_chunk = [&](const float (&hin)[H], const float (&d)[H]) {
-      if (job >= 1) flush(job - 1);
+      if (job >= 2) flush(job - 2);
       const long long ts0 = PROF ? clock64() : 0;
       const int64_t gi = job * 8 + warp;  // staging chunk counter
       stage_acquire(st_empty, gi);
@@ -376,7 +372,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     auto write_db = [&](const float (&d)[H]) {
       const long long t0 = PROF ? clock64() : 0;
       const float2 cs = warp_colsum64(d);
-      float* dst = dbp + ((job % 3) * 8 + warp) * 64 + colsum_base(lane);
+      float* dst = dbp + ((job % 4) * 8 + warp) * 64 + colsum_base(lane);
       dst[0] = cs.x;
       dst[1] = cs.y;
       if (PROF) pf[4] += (unsigned long long)(clock64() - t0);
@@ -540,7 +536,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       }
       if (PROF) pf[7] += (unsigned long long)(clock64() - ti0);
     }
-    if (job >= 1) flush(job - 1);  // last dW job of this CTA
+    if (job >= 2) flush(job - 2);  // last two dW jobs of this CTA
+    if (job >= 1) flush(job - 1);
     if (PROF && warp == 0 && lane == 0) {
       pf[0] = (unsigned long long)(clock64() - pf_t0);
 #pragma unroll
@@ -552,10 +549,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     const uint32_t tm = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t*>(tmem_base_slot), 0);
     {
       constexpr uint32_t idesc = ptx::idesc_tf32(128, H);
-      constexpr uint32_t idesc_dw = ptx::idesc_tf32(128, 2 * H) | (1u << 15) | (1u << 16);  // A, B MN-major
       int ws = 0;
-      uint32_t wph = 0, pa[2] = {0, 0}, pdw = 0;
-      int64_t gi = 0;  // staging chunk counter
+      uint32_t wph = 0, pa[2] = {0, 0};
       auto mma3 = [&](int s, uint32_t bbase, bool first_zero) {
         const uint32_t slot = ptx::opaque(tm + s * Cfg::SLOT_COLS);
         // descriptor start addresses advance in 16-byte units: bump the encoded
@@ -570,7 +565,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           ptx::mma_tf32_ts_w(slot + 2 * H, slot + H + 8 * ks, b_hi, idesc, 1u);
         }
       };
-      unsigned long long pc_w = 0, pc_a = 0, pc_st = 0, pc_dw = 0;  // wait cycles (profiling only)
+      unsigned long long pc_w = 0, pc_a = 0;  // wait cycles (profiling only)
       const long long t_start = clock64();
       auto timed_wait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
         if (!PROF) {
@@ -593,32 +588,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           wph ^= 1;
         }
       };
-      unsigned long long pc_fwd = 0, pc_dwt = 0, pc_mma = 0;  // phase cycles (profiling only)
-      auto dw_job = [&]() {
-        const long long t_dw0 = PROF ? clock64() : 0;
-        timed_wait(dw_empty, pdw ^ 1, pc_dw);
-        ptx::tc_fence_after();
-        for (int b = 0; b < 8; ++b, ++gi) {
-          const int buf = (int)(gi % Cfg::NSTAGE);
-          const uint32_t par = (uint32_t)((gi / Cfg::NSTAGE) & 1);
-          timed_wait(&st_full[buf], par, pc_st);
-          ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(stage + (size_t)buf * Cfg::STAGE_BYTES);
-          constexpr uint64_t swz = (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
-          const uint64_t a0 = ptx::opaque64(ptx::smem_desc(sa, Cfg::ST_LBO, Cfg::ST_SBO) | swz);
-          const uint32_t t_dw = ptx::opaque(tm + Cfg::DW_COL);
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ad = a0 + (uint64_t)((ks * 2 * Cfg::ST_SBO) >> 4);
-            const uint64_t bd = ad + (uint64_t)(16384 >> 4);
-            ptx::mma_tf32_ss_w(t_dw, ad, bd, idesc_dw, (b > 0 || ks > 0) ? 1u : 0u);
-          }
-          ptx::mma_commit_w(&st_empty[((gi / Cfg::NSTAGE) & 1) * Cfg::NSTAGE + buf]);
-        }
-        ptx::mma_commit_w(dw_full);
-        pdw ^= 1;
-        if (PROF) pc_dwt += (unsigned long long)(clock64() - t_dw0);
-      };
+      unsigned long long pc_fwd = 0, pc_mma = 0;  // phase cycles (profiling only)
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
         const long long t_p0 = PROF ? clock64() : 0;
         // forward recompute: input chunks then hidden blocks (no output linear)
@@ -659,9 +629,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             if (PROF) pc_mma += (unsigned long long)(clock64() - t_m0);
           }
           release_w();
-          dw_job();
         }
-        // input linear: per segment, dX then dW
+        // input linear: per segment, dX (dW on the dW issuer)
         for (int c = 0; c < nseg; ++c) {
           const uint32_t bb = next_w();
           for (int s = 0; s < 2; ++s) {
@@ -672,23 +641,66 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             ptx::mma_commit_w(&d_full[s]);
           }
           release_w();
-          dw_job();
         }
       }
       if (PROF && lane == 0) {
         atomicAdd(a.prof + kProfTotal, (unsigned long long)(clock64() - t_start));
         atomicAdd(a.prof + kProfW, pc_w);
         atomicAdd(a.prof + kProfA, pc_a);
-        atomicAdd(a.prof + kProfSt, pc_st);
-        atomicAdd(a.prof + kProfDwE, pc_dw);
         atomicAdd(a.prof + kProfFwd, pc_fwd);
-        atomicAdd(a.prof + kProfDw, pc_dwt);
         atomicAdd(a.prof + kProfMma, pc_mma);
       }
     }
+  } else if (warp == 9) {
+    // ================================================================ dW issuer
+    // Separate instruction stream from the dX issuer, so the dX MMAs of one
+    // slot never wait behind the other slot's staging of the current job.
+    const uint32_t tm = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t*>(tmem_base_slot), 0);
+    constexpr uint32_t idesc_dw = ptx::idesc_tf32(128, H) | (1u << 15) | (1u << 16);  // A, B MN-major, N = 64
+    int64_t gi = 0;  // staging chunk counter
+    unsigned long long pc_st = 0, pc_dw = 0, pc_dwt = 0;
+    const long long t_start = PROF ? clock64() : 0;
+    const int64_t n_jobs = ((n_pairs - blockIdx.x + gridDim.x - 1) / gridDim.x) * n_dw;
+    for (int64_t jd = 0; jd < n_jobs; ++jd) {
+      const int acc = (int)(jd & 1);
+      const long long t0 = PROF ? clock64() : 0;
+      ptx::mbar_wait(&dw_empty[acc], (uint32_t)(((jd >> 1) & 1) ^ 1));  // job jd - 2 drained
+      ptx::tc_fence_after();
+      if (PROF) pc_dw += (unsigned long long)(clock64() - t0);
+      const uint32_t t_dw = ptx::opaque(tm + Cfg::DW_COL + 64 * acc);
+      for (int b = 0; b < 8; ++b, ++gi) {
+        const int buf = (int)(gi % Cfg::NSTAGE);
+        const uint32_t par = (uint32_t)((gi / Cfg::NSTAGE) & 1);
+        const long long t1 = PROF ? clock64() : 0;
+        ptx::mbar_wait(&st_full[buf], par);
+        ptx::tc_fence_after();
+        if (PROF) pc_st += (unsigned long long)(clock64() - t1);
+        const uint32_t sa = ptx::smem_u32(stage + (size_t)buf * Cfg::STAGE_BYTES);
+        constexpr uint64_t swz = (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+        const uint64_t a0 = ptx::opaque64(ptx::smem_desc(sa, Cfg::ST_LBO, Cfg::ST_SBO) | swz);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          // [h_hi ; h_lo] (M = 128) x d_hi and x d_lo (N = 64 each, MN atoms 0-1 / 2-3)
+          const uint64_t ad = a0 + (uint64_t)((ks * 2 * Cfg::ST_SBO) >> 4);
+          const uint64_t bd_hi = ad + (uint64_t)(16384 >> 4);
+          const uint64_t bd_lo = bd_hi + (uint64_t)((2 * Cfg::ST_LBO) >> 4);
+          ptx::mma_tf32_ss_w(t_dw, ad, bd_hi, idesc_dw, (b > 0 || ks > 0) ? 1u : 0u);
+          ptx::mma_tf32_ss_w(t_dw, ad, bd_lo, idesc_dw, 1u);
+        }
+        ptx::mma_commit_w(&st_empty[((gi / Cfg::NSTAGE) & 1) * Cfg::NSTAGE + buf]);
+      }
+      ptx::mma_commit_w(&dw_full[acc]);
+      if (PROF) pc_dwt += (unsigned long long)(clock64() - t0);
+    }
+    if (PROF && lane == 0) {
+      (void)t_start;
+      atomicAdd(a.prof + kProfSt, pc_st);
+      atomicAdd(a.prof + kProfDwE, pc_dw);
+      atomicAdd(a.prof + kProfDw, pc_dwt);
+    }
   } else {
-    // ================================================================ loader (warp 9; 10-11 idle)
-    if (warp == 9 && lane == 0) {
+    // ================================================================ loader (warp 10; 11 idle)
+    if (warp == 10 && lane == 0) {
       int ws = 0;
       uint32_t wph = 0;
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
