@@ -29,6 +29,7 @@ enum {
   HGNN_ERR_INTEGRITY = 5,      /* IntegrityError */
   HGNN_ERR_UNINITIALIZED = 6,  /* UninitializedError */
   HGNN_ERR_SIZE = 7,           /* SizeError */
+  HGNN_ERR_OPTIMIZER = 8,      /* OptimizerError */
   HGNN_ERR_CUDA = 20,          /* device fault / missing GPU */
   HGNN_ERR_NCCL = 21,          /* NCCL failure */
   HGNN_ERR_INTERNAL = 22
@@ -160,6 +161,32 @@ int hgnn_set_inputs(hgnn_ctx* ctx, const double* x0, const double* e0, const dou
 int hgnn_mp_step_device(hgnn_ctx* ctx);
 /* Device gradients -> host (fp64), same layout as hgnn_params_upload. */
 int hgnn_get_grads(hgnn_ctx* ctx, double* mp_grads);
+
+/* ========================================================================== */
+/* Model level: node / edge encoders and the decoder on  */
+/* the device around the MP stack, the consistent loss, rank-averaged          */
+/* gradients and Adam — compute_gradients / train_step (model.cpp:556-579).   */
+/* Hidden width 64, feature widths (F_x, F_e, F_y) = (3, 7, 3).               */
+/* ========================================================================== */
+/* After hgnn_configure: feature widths (GnnConfig in_node_dim, in_edge_dim, out_dim). */
+int hgnn_model_configure(hgnn_ctx* ctx, int64_t in_node_dim, int64_t in_edge_dim, int64_t out_dim);
+/* Length of the full ModelParams::for_each vector (model.cpp:124-135), -1 before configure. */
+int64_t hgnn_model_param_count(hgnn_ctx* ctx);
+/* Full parameter vector, fp64, for_each order; resets the Adam state. */
+int hgnn_model_params_upload(hgnn_ctx* ctx, const double* params, int64_t count);
+int hgnn_model_params_download(hgnn_ctx* ctx, double* params);
+/* node_features: rows x F_x (ReducedGraph::node_features), edge_features:
+ * N_e x F_e in edge-id order (init_edge_features), target: num_local x F_y or
+ * NULL for the autoencoding target (model.cpp:605-607). Needs node_inv_degree
+ * in the uploaded graph (consistent-loss weights). */
+int hgnn_model_set_data(hgnn_ctx* ctx, const double* node_features, const double* edge_features, const double* target);
+/* compute_gradients (model.cpp:556-567): loss (all ranks), gradients averaged
+ * over ranks in for_each order (nullable), decoder output y (num_local x F_y,
+ * nullable). Collective over all ranks. */
+int hgnn_compute_gradients(hgnn_ctx* ctx, double* loss, double* grads, double* y);
+/* train_step (model.cpp:569-579): compute_gradients + bias-corrected Adam
+ * (nn.cpp:331-360) on fp64 master parameters; returns the loss before the update. */
+int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double eps, double* loss);
 
 /* ---- options --------------------------------------------------------------- */
 /* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),

@@ -193,6 +193,9 @@ def ref_lib() -> C.CDLL:
         lib.ref_run_size.restype = C.c_int64
         lib.ref_run_size.argtypes = [vp, C.c_int, C.c_int, C.c_int]
         lib.ref_run_export.argtypes = [vp, C.c_int, C.c_int, C.c_int, f64p]
+        lib.ref_train.restype = C.c_int
+        lib.ref_train.argtypes = [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_uint64, C.c_int64, C.c_double,
+                                  C.c_double, C.c_double, C.c_double, C.c_int, f64p, f64p]
         _rlib = lib
     return _rlib
 
@@ -320,3 +323,16 @@ def ref_run(graph: RefGraph, H, M, k, mode, seed=0, params=None, threads_per_ran
         params = np.ascontiguousarray(params, dtype=np.float64)
         p = params.ctypes.data_as(f64p)
     return RefRun(lib.ref_run(graph.h, H, M, k, MODES[mode], seed, p, threads_per_rank), H)
+
+
+def ref_train(graph: RefGraph, H, M, k, mode, seed, iters, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
+              threads_per_rank=0):
+    """Reference train() (model.cpp:582-640): per-iteration losses and rank 0's final parameters."""
+    lib = ref_lib()
+    losses = np.zeros(iters)
+    params = np.zeros(lib.ref_param_count(H, M, k))
+    rc = lib.ref_train(graph.h, H, M, k, MODES[mode], seed, iters, lr, beta1, beta2, eps, threads_per_rank,
+                       losses.ctypes.data_as(f64p), params.ctypes.data_as(f64p))
+    if rc != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return losses, params

@@ -408,6 +408,33 @@ void* ref_run(void* graph, int64_t H, int64_t M, int64_t k, int mode, uint64_t s
   return rc == 0 ? out : nullptr;
 }
 
+// train (model.cpp:582-640) for `iters` Adam steps on the graph's TGV
+// features (autoencoding), params from init_params(seed); losses[it] and the
+// final parameters of rank 0 (for_each order). audit off.
+int ref_train(void* graph, int64_t H, int64_t M, int64_t k, int mode, uint64_t seed, int64_t iters, double lr,
+              double beta1, double beta2, double eps, int threads_per_rank, double* losses, double* final_params) {
+  return guarded([&] {
+    const DistributedGraph& dg = static_cast<RefGraph*>(graph)->dg;
+    const int64_t R = dg.num_ranks();
+    std::vector<ModelParams> per_rank(static_cast<size_t>(R), init_params(make_cfg(H, M, k, mode), seed));
+    TrainConfig tc;
+    tc.adam.lr = lr;
+    tc.adam.beta1 = beta1;
+    tc.adam.beta2 = beta2;
+    tc.adam.eps = eps;
+    tc.iterations = iters;
+    tc.audit_interval = 0;
+    RankRuntime rt(R, threads_per_rank);
+    const auto recs = train(rt, per_rank, dg, {}, tc);
+    for (int64_t i = 0; i < iters; ++i) losses[i] = recs[static_cast<size_t>(i)].loss;
+    int64_t off = 0;
+    per_rank[0].for_each([&](const std::string&, Tensor2D& t) {
+      std::memcpy(final_params + off, t.data(), sizeof(double) * static_cast<size_t>(t.size()));
+      off += t.size();
+    });
+  });
+}
+
 void ref_run_free(void* run) { delete static_cast<RefRun*>(run); }
 double ref_run_loss(void* run) { return static_cast<RefRun*>(run)->loss; }
 void ref_run_times(void* run, double* fwd_ms, double* bwd_ms) {

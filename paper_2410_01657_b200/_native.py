@@ -45,12 +45,16 @@ class SizeError(Error):
     pass
 
 
+class OptimizerError(Error):
+    """hgnn::OptimizerError (error.hpp:51-55)."""
+
+
 class DeviceError(Error):
     """CUDA / NCCL failure or missing B200."""
 
 
 _CODES = {1: ShapeError, 2: ConfigError, 3: PartitionError, 4: CollectiveError, 5: IntegrityError,
-          6: UninitializedError, 7: SizeError, 20: DeviceError, 21: DeviceError, 22: Error}
+          6: UninitializedError, 7: SizeError, 8: OptimizerError, 20: DeviceError, 21: DeviceError, 22: Error}
 
 MODE_NONE, MODE_A2A, MODE_NA2A = 0, 1, 2
 MODES = {"none": MODE_NONE, "a2a": MODE_A2A, "na2a": MODE_NA2A}
@@ -133,6 +137,13 @@ def _load() -> C.CDLL:
         "hgnn_debug_profile": (C.c_int, [vp, C.c_void_p]),
         "hgnn_bench_mma": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
         "hgnn_bench_alu": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+        "hgnn_model_configure": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64]),
+        "hgnn_model_param_count": (C.c_int64, [vp]),
+        "hgnn_model_params_upload": (C.c_int, [vp, f64p, C.c_int64]),
+        "hgnn_model_params_download": (C.c_int, [vp, f64p]),
+        "hgnn_model_set_data": (C.c_int, [vp, f64p, f64p, f64p]),
+        "hgnn_compute_gradients": (C.c_int, [vp, C.POINTER(C.c_double), f64p, f64p]),
+        "hgnn_train_step": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
         "hgnn_kernel_timing": (C.c_int, [vp, C.c_int]),
         "hgnn_kernel_time": (C.c_int, [vp, C.c_int, f64p, i64p]),
         "hgnn_launch_count": (C.c_int64, [vp, C.c_int]),
@@ -151,7 +162,9 @@ EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_grap
             "hgnn_ctx_create", "hgnn_ctx_destroy", "hgnn_ctx_stream", "hgnn_graph_upload", "hgnn_configure",
             "hgnn_params_upload", "hgnn_mp_forward", "hgnn_mp_backward", "hgnn_get_trace",
             "hgnn_synthetic_inputs", "hgnn_set_inputs", "hgnn_mp_step_device", "hgnn_get_grads",
-            "hgnn_set_option", "hgnn_selftest_mma", "hgnn_bench_mma", "hgnn_bench_alu", "hgnn_debug_profile", "hgnn_kernel_timing", "hgnn_kernel_time", "hgnn_launch_count", "hgnn_halo_bytes"]
+            "hgnn_set_option", "hgnn_selftest_mma", "hgnn_bench_mma", "hgnn_bench_alu", "hgnn_model_configure", "hgnn_model_param_count",
+            "hgnn_model_params_upload", "hgnn_model_params_download", "hgnn_model_set_data", "hgnn_compute_gradients",
+            "hgnn_train_step", "hgnn_debug_profile", "hgnn_kernel_timing", "hgnn_kernel_time", "hgnn_launch_count", "hgnn_halo_bytes"]
 
 
 def check(status: int) -> None:

@@ -1,0 +1,421 @@
+// Encoder / decoder MLPs (SIMT fp32, sm_100a): the row-wise MLPs on either
+// side of the message-passing stack.
+//
+// Spec (nn.hpp:27-58, model.cpp:70-101), H = 64 hidden width, k hidden blocks:
+//   h = x W0 + b0;  h += ELU(LN0(h Wj + bj)), j = 1..k;
+//   y = h W_{k+1} + b_{k+1} (+ x W_skip);  y = LN(y) * gamma + beta (encoders)
+// encoder: IN = F_x or F_e, OUT = H, skip + output LayerNorm (model.cpp:70-80)
+// decoder: IN = H, OUT = F_y, skip, no LayerNorm (model.cpp:92-101)
+// Parameters in MlpParams::for_each order (nn.cpp:38-46): w0, b0, ..., w_{k+1},
+// b_{k+1}, skip, [ln_g, ln_b]; fp32 copies, staged whole in shared memory.
+//
+// One thread owns one row. The backward recomputes the forward per row and
+// keeps the per-row intermediates (hidden states, normed values, inverse
+// standard deviations, pre-LayerNorm output) in a per-CTA global scratch
+// ([slot][row] layout: coalesced). Weight gradients are reduced over a tile
+// of kGenThreads rows through shared memory — every (i, j) element summed
+// by one owning thread in row order — and added to a per-CTA partial owned
+// by that thread, so the result is deterministic run to run.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tc_ptx.cuh"
+
+namespace hgnn_b200 {
+
+constexpr int kGenThreads = 128;
+constexpr int kGenH = 64;
+
+__host__ __device__ inline int64_t gen_param_count(int in_dim, int out_dim, int k, bool skip, bool out_ln) {
+  const int H = kGenH;
+  return (int64_t)in_dim * H + H + (int64_t)k * (H * H + H) + (int64_t)H * out_dim + out_dim +
+         (skip ? (int64_t)in_dim * out_dim : 0) + (out_ln ? 2 * out_dim : 0);
+}
+
+// Offsets (floats) inside one MLP's for_each block.
+struct GenLayout {
+  int in_dim, out_dim, k;
+  __host__ __device__ int64_t w(int l) const {  // l = 0 .. k+1
+    const int H = kGenH;
+    return l == 0 ? 0 : (int64_t)in_dim * H + H + (int64_t)(l - 1) * (H * H + H);
+  }
+  __host__ __device__ int64_t b(int l) const {
+    const int H = kGenH;
+    return w(l) + (l == 0 ? (int64_t)in_dim * H : (l <= k ? (int64_t)H * H : (int64_t)H * out_dim));
+  }
+  __host__ __device__ int64_t skip() const { return b(k + 1) + out_dim; }
+  __host__ __device__ int64_t ln_g() const { return skip() + (int64_t)in_dim * out_dim; }
+  __host__ __device__ int64_t ln_b() const { return ln_g() + out_dim; }
+};
+
+struct GenArgs {
+  int64_t n_rows;
+  const float* in;        // n_rows x IN
+  float* out;             // n_rows x OUT (forward)
+  const float* d_out;     // n_rows x OUT (backward)
+  float* d_in;            // n_rows x IN input adjoint (backward, decoder only)
+  const float* params;    // fp32, for_each layout
+  float* grad_partial;    // [gridDim.x][n_par] fp32 (backward)
+  float* scratch;         // [gridDim.x][slots][kGenThreads] (backward)
+  int k;
+  int64_t n_par;
+};
+
+__device__ __forceinline__ float gen_elu(float z) { return z > 0.f ? z : ptx::exp_fast(z) - 1.0f; }
+
+// Two-pass LayerNorm statistics of N values (kernels.cpp:81-94).
+template <int N>
+__device__ __forceinline__ void gen_ln_stats(const float (&v)[N], float& mean, float& inv_std) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) s += v[j];
+  mean = s * (1.0f / N);
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float d = v[j] - mean;
+    q = fmaf(d, d, q);
+  }
+  inv_std = ptx::rsqrt_fast(q * (1.0f / N) + 1e-12f);
+}
+
+// acc[j] += sum_t v[t] W[t*NO + j] (W row-major, shared memory, warp-uniform reads)
+template <int NI, int NO>
+__device__ __forceinline__ void gen_gemv(float (&acc)[NO], const float (&v)[NI], const float* __restrict__ W) {
+#pragma unroll
+  for (int t = 0; t < NI; ++t) {
+    const float vt = v[t];
+    if (NO % 4 == 0) {
+      const float4* w4 = reinterpret_cast<const float4*>(W + t * NO);
+#pragma unroll
+      for (int j = 0; j < NO / 4; ++j) {
+        const float4 w = w4[j];
+        acc[4 * j] = fmaf(vt, w.x, acc[4 * j]);
+        acc[4 * j + 1] = fmaf(vt, w.y, acc[4 * j + 1]);
+        acc[4 * j + 2] = fmaf(vt, w.z, acc[4 * j + 2]);
+        acc[4 * j + 3] = fmaf(vt, w.w, acc[4 * j + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NO; ++j) acc[j] = fmaf(vt, W[t * NO + j], acc[j]);
+    }
+  }
+}
+
+// acc[t] += sum_j d[j] W[t*NO + j]  (adjoint product d W^T)
+template <int NI, int NO>
+__device__ __forceinline__ void gen_gemv_t(float (&acc)[NI], const float (&d)[NO], const float* __restrict__ W) {
+#pragma unroll
+  for (int t = 0; t < NI; ++t) {
+    float s = 0.f;
+    if (NO % 4 == 0) {
+      const float4* w4 = reinterpret_cast<const float4*>(W + t * NO);
+#pragma unroll
+      for (int j = 0; j < NO / 4; ++j) {
+        const float4 w = w4[j];
+        s = fmaf(d[4 * j], w.x, s);
+        s = fmaf(d[4 * j + 1], w.y, s);
+        s = fmaf(d[4 * j + 2], w.z, s);
+        s = fmaf(d[4 * j + 3], w.w, s);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NO; ++j) s = fmaf(d[j], W[t * NO + j], s);
+    }
+    acc[t] += s;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void gen_load_row(float (&v)[N], const float* __restrict__ src, bool valid) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = valid ? __ldg(src + j) : 0.f;
+}
+
+__device__ __forceinline__ void gen_stage_params(float* dst, const float* __restrict__ src, int64_t n) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+// ------------------------------------------------------------------ forward
+template <int IN, int OUT, bool SKIP, bool OUT_LN>
+__global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a) {
+  constexpr int H = kGenH;
+  extern __shared__ __align__(16) float gsm[];
+  const GenLayout L{IN, OUT, a.k};
+  gen_stage_params(gsm, a.params, a.n_par);
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * kGenThreads + threadIdx.x; row - threadIdx.x < a.n_rows;
+       row += (int64_t)gridDim.x * kGenThreads) {
+    const bool valid = row < a.n_rows;
+    float h[H];
+    {
+      float x[IN];
+      gen_load_row<IN>(x, a.in + row * IN, valid);
+#pragma unroll
+      for (int j = 0; j < H; ++j) h[j] = gsm[L.b(0) + j];
+      gen_gemv<IN, H>(h, x, gsm + L.w(0));
+    }
+    for (int l = 1; l <= a.k; ++l) {
+      float u[H];
+#pragma unroll
+      for (int j = 0; j < H; ++j) u[j] = gsm[L.b(l) + j];
+      gen_gemv<H, H>(u, h, gsm + L.w(l));
+      float mean, inv_std;
+      gen_ln_stats<H>(u, mean, inv_std);
+#pragma unroll
+      for (int j = 0; j < H; ++j) h[j] += gen_elu((u[j] - mean) * inv_std);
+    }
+    float y[OUT];
+#pragma unroll
+    for (int j = 0; j < OUT; ++j) y[j] = gsm[L.b(a.k + 1) + j];
+    gen_gemv<H, OUT>(y, h, gsm + L.w(a.k + 1));
+    if (SKIP) {
+      float x[IN];
+      gen_load_row<IN>(x, a.in + row * IN, valid);
+      gen_gemv<IN, OUT>(y, x, gsm + L.skip());
+    }
+    if (OUT_LN) {
+      float mean, inv_std;
+      gen_ln_stats<OUT>(y, mean, inv_std);
+#pragma unroll
+      for (int j = 0; j < OUT; ++j) y[j] = gsm[L.ln_g() + j] * ((y[j] - mean) * inv_std) + gsm[L.ln_b() + j];
+    }
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < OUT; ++j) a.out[row * OUT + j] = y[j];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ backward
+// Scratch slots per row: hidden states h_0..h_k (k+1) x H, normed t_1..t_k
+// k x H, inv_std k, pre-LayerNorm output OUT (+ mean / inv_std 2).
+__host__ __device__ inline int64_t gen_scratch_slots(int k, int out_dim) {
+  return (int64_t)(2 * k + 1) * kGenH + k + out_dim + 2;
+}
+
+// Tile reduction of dW += sum_rows A[r][i] D[r][j] for NI x NO, A / D staged
+// in shared memory as [i][row] / [j][row]; thread t owns elements t, t + T, ...
+template <int NI, int NO>
+__device__ __forceinline__ void gen_dw_tile(float* __restrict__ gp, const float* __restrict__ sa,
+                                            const float* __restrict__ sd) {
+  for (int e = threadIdx.x; e < NI * NO; e += kGenThreads) {
+    const int i = e / NO, j = e % NO;
+    const float* ar = sa + i * kGenThreads;
+    const float* dr = sd + j * kGenThreads;
+    float s = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < kGenThreads; ++r) s = fmaf(ar[r], dr[r], s);
+    gp[e] += s;
+  }
+}
+template <int NO>
+__device__ __forceinline__ void gen_db_tile(float* __restrict__ gp, const float* __restrict__ sd) {
+  for (int j = threadIdx.x; j < NO; j += kGenThreads) {
+    const float* dr = sd + j * kGenThreads;
+    float s = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < kGenThreads; ++r) s += dr[r];
+    gp[j] += s;
+  }
+}
+template <int N>
+__device__ __forceinline__ void gen_stage_col(float* s, const float (&v)[N]) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) s[j * kGenThreads + threadIdx.x] = v[j];
+}
+
+// smem: params | A stage (64 x T) | D stage (64 x T)
+template <int IN, int OUT, bool SKIP, bool OUT_LN, bool DIN>
+__global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a) {
+  constexpr int H = kGenH;
+  extern __shared__ __align__(16) float gsm[];
+  const GenLayout L{IN, OUT, a.k};
+  const int K = a.k;
+  float* sA = gsm + ((a.n_par + 3) / 4) * 4;
+  float* sD = sA + H * kGenThreads;
+  gen_stage_params(gsm, a.params, a.n_par);
+  float* gp = a.grad_partial + (int64_t)blockIdx.x * a.n_par;
+  const int64_t slots = gen_scratch_slots(K, OUT);
+  float* scr = a.scratch + (int64_t)blockIdx.x * slots * kGenThreads + threadIdx.x;
+  auto S = [&](int64_t slot) -> float& { return scr[slot * kGenThreads]; };
+  const int64_t s_h = 0, s_t = (int64_t)(K + 1) * H, s_inv = s_t + (int64_t)K * H, s_y = s_inv + K,
+                s_yst = s_y + OUT;
+  __syncthreads();
+  for (int64_t row0 = (int64_t)blockIdx.x * kGenThreads; row0 < a.n_rows; row0 += (int64_t)gridDim.x * kGenThreads) {
+    const int64_t row = row0 + threadIdx.x;
+    const bool valid = row < a.n_rows;
+    // ---- forward recompute, keeping the intermediates
+    {
+      float h[H];
+      {
+        float x[IN];
+        gen_load_row<IN>(x, a.in + row * IN, valid);
+#pragma unroll
+        for (int j = 0; j < H; ++j) h[j] = gsm[L.b(0) + j];
+        gen_gemv<IN, H>(h, x, gsm + L.w(0));
+      }
+#pragma unroll
+      for (int j = 0; j < H; ++j) S(s_h + j) = h[j];
+      for (int l = 1; l <= K; ++l) {
+        float u[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) u[j] = gsm[L.b(l) + j];
+        gen_gemv<H, H>(u, h, gsm + L.w(l));
+        float mean, inv_std;
+        gen_ln_stats<H>(u, mean, inv_std);
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+          const float t = (u[j] - mean) * inv_std;
+          S(s_t + (int64_t)(l - 1) * H + j) = t;
+          h[j] += gen_elu(t);
+          S(s_h + (int64_t)l * H + j) = h[j];
+        }
+        S(s_inv + l - 1) = inv_std;
+      }
+      float y[OUT];
+#pragma unroll
+      for (int j = 0; j < OUT; ++j) y[j] = gsm[L.b(K + 1) + j];
+      gen_gemv<H, OUT>(y, h, gsm + L.w(K + 1));
+      if (SKIP) {
+        float x[IN];
+        gen_load_row<IN>(x, a.in + row * IN, valid);
+        gen_gemv<IN, OUT>(y, x, gsm + L.skip());
+      }
+      if (OUT_LN) {
+        float mean, inv_std;
+        gen_ln_stats<OUT>(y, mean, inv_std);
+#pragma unroll
+        for (int j = 0; j < OUT; ++j) S(s_y + j) = (y[j] - mean) * inv_std;  // xhat
+        S(s_yst) = inv_std;
+      }
+    }
+    // ---- output adjoint, output LayerNorm (kernels.cpp:99-126 with gamma)
+    float dy[OUT];
+    gen_load_row<OUT>(dy, a.d_out + row * OUT, valid);
+    if (OUT_LN) {
+      float xh[OUT];
+#pragma unroll
+      for (int j = 0; j < OUT; ++j) xh[j] = S(s_y + j);
+      // d gamma += dy * xhat, d beta += dy (tile-reduced below)
+      float gdy[OUT], gm = 0.f, gxm = 0.f;
+#pragma unroll
+      for (int j = 0; j < OUT; ++j) {
+        gdy[j] = gsm[L.ln_g() + j] * dy[j];
+        gm += gdy[j];
+        gxm = fmaf(gdy[j], xh[j], gxm);
+      }
+      gm *= 1.0f / OUT;
+      gxm *= 1.0f / OUT;
+      const float inv_std = S(s_yst);
+      __syncthreads();
+      {
+        float prod[OUT];
+#pragma unroll
+        for (int j = 0; j < OUT; ++j) prod[j] = dy[j] * xh[j];
+        gen_stage_col<OUT>(sA, prod);
+        gen_stage_col<OUT>(sD, dy);
+      }
+      __syncthreads();
+      gen_db_tile<OUT>(gp + L.ln_g(), sA);
+      gen_db_tile<OUT>(gp + L.ln_b(), sD);
+#pragma unroll
+      for (int j = 0; j < OUT; ++j) dy[j] = (gdy[j] - gm - xh[j] * gxm) * inv_std;
+    }
+    // ---- output projection (nn.cpp:241-245) and skip (nn.cpp:247-254)
+    float dh[H];
+    {
+      float hk[H];
+#pragma unroll
+      for (int j = 0; j < H; ++j) hk[j] = S(s_h + (int64_t)K * H + j);
+      __syncthreads();
+      gen_stage_col<H>(sA, hk);
+      gen_stage_col<OUT>(sD, dy);
+      __syncthreads();
+      gen_dw_tile<H, OUT>(gp + L.w(K + 1), sA, sD);
+      gen_db_tile<OUT>(gp + L.b(K + 1), sD);
+      if (SKIP) {
+        float x[IN];
+        gen_load_row<IN>(x, a.in + row * IN, valid);
+        __syncthreads();
+        gen_stage_col<IN>(sA, x);
+        __syncthreads();
+        gen_dw_tile<IN, OUT>(gp + L.skip(), sA, sD);
+      }
+#pragma unroll
+      for (int j = 0; j < H; ++j) dh[j] = 0.f;
+      gen_gemv_t<H, OUT>(dh, dy, gsm + L.w(K + 1));
+    }
+
+    // ---- hidden blocks in reverse (nn.cpp:259-274)
+    for (int l = K; l >= 1; --l) {
+      float du[H];
+      float gm = 0.f, gxm = 0.f;
+#pragma unroll
+      for (int j = 0; j < H; ++j) {
+        const float t = S(s_t + (int64_t)(l - 1) * H + j);
+        du[j] = dh[j] * (t > 0.f ? 1.0f : ptx::exp_fast(t));  // elu', kernels.cpp:68-71
+        gm += du[j];
+        gxm = fmaf(du[j], t, gxm);
+      }
+      gm *= 1.0f / H;
+      gxm *= 1.0f / H;
+      const float inv_std = S(s_inv + l - 1);
+#pragma unroll
+      for (int j = 0; j < H; ++j) du[j] = (du[j] - gm - S(s_t + (int64_t)(l - 1) * H + j) * gxm) * inv_std;
+      {
+        float hp[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) hp[j] = S(s_h + (int64_t)(l - 1) * H + j);
+        __syncthreads();
+        gen_stage_col<H>(sA, hp);
+        gen_stage_col<H>(sD, du);
+        __syncthreads();
+      }
+      gen_dw_tile<H, H>(gp + L.w(l), sA, sD);
+      gen_db_tile<H>(gp + L.b(l), sD);
+      gen_gemv_t<H, H>(dh, du, gsm + L.w(l));  // d_prev = d_u W^T + d_h
+    }
+    // ---- input projection (nn.cpp:277-281)
+    if (DIN) {  // d_in = d_h W0^T (+ d_y W_skip^T), 16 input columns at a time
+#pragma unroll
+      for (int c = 0; c < IN; c += 16) {
+        float din[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          float s = 0.f;
+          if (c + t < IN) {
+            const float* w0 = gsm + L.w(0) + (int64_t)(c + t) * H;
+#pragma unroll
+            for (int j = 0; j < H; ++j) s = fmaf(dh[j], w0[j], s);
+            if (SKIP) {
+              const float* ws = gsm + L.skip() + (int64_t)(c + t) * OUT;
+#pragma unroll
+              for (int j = 0; j < OUT; ++j) s = fmaf(dy[j], ws[j], s);
+            }
+          }
+          din[t] = s;
+        }
+        if (valid) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c + t < IN) a.d_in[row * IN + c + t] = din[t];
+        }
+      }
+    }
+    {
+      float x[IN];
+      gen_load_row<IN>(x, a.in + row * IN, valid);
+      __syncthreads();
+      gen_stage_col<IN>(sA, x);
+      gen_stage_col<H>(sD, dh);
+      __syncthreads();
+      gen_dw_tile<IN, H>(gp + L.w(0), sA, sD);
+      gen_db_tile<H>(gp + L.b(0), sD);
+    }
+  }
+}
+
+}  // namespace hgnn_b200

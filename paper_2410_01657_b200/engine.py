@@ -123,6 +123,45 @@ class Engine:
         N.check(N.LIB.hgnn_get_trace(self._h, layer, sel, out.ctypes.data_as(N.f64p)))
         return out
 
+    # ---- model level: encoders + MP stack + decoder, loss, Adam --
+    def model_configure(self, in_node_dim: int = 3, in_edge_dim: int = 7, out_dim: int = 3) -> int:
+        N.check(N.LIB.hgnn_model_configure(self._h, in_node_dim, in_edge_dim, out_dim))
+        self.model_dims = (in_node_dim, in_edge_dim, out_dim)
+        return int(N.LIB.hgnn_model_param_count(self._h))
+
+    def model_params_upload(self, params: np.ndarray) -> None:
+        a, p = _f64(params)
+        N.check(N.LIB.hgnn_model_params_upload(self._h, p, a.size))
+
+    def model_params(self) -> np.ndarray:
+        out = np.empty(int(N.LIB.hgnn_model_param_count(self._h)))
+        N.check(N.LIB.hgnn_model_params_download(self._h, out.ctypes.data_as(N.f64p)))
+        return out
+
+    def model_set_data(self, node_features: np.ndarray, edge_features: np.ndarray, target=None) -> None:
+        g = self.graph
+        fx, fe, fy = self.model_dims
+        _, xp = _f64(node_features, (g.rows, fx))
+        _, ep = _f64(edge_features, (g.num_edges, fe))
+        _, tp = _f64(target, (g.num_local, fy))
+        N.check(N.LIB.hgnn_model_set_data(self._h, xp, ep, tp))
+
+    def compute_gradients(self):
+        """compute_gradients (model.cpp:556-567): (loss, rank-averaged grads, y)."""
+        g = self.graph
+        loss = C.c_double()
+        grads = np.empty(int(N.LIB.hgnn_model_param_count(self._h)))
+        y = np.empty((g.num_local, self.model_dims[2]))
+        N.check(N.LIB.hgnn_compute_gradients(self._h, C.byref(loss), grads.ctypes.data_as(N.f64p),
+                                             y.ctypes.data_as(N.f64p)))
+        return loss.value, grads, y
+
+    def train_step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> float:
+        """train_step (model.cpp:569-579): loss before the Adam update."""
+        loss = C.c_double()
+        N.check(N.LIB.hgnn_train_step(self._h, lr, beta1, beta2, eps, C.byref(loss)))
+        return loss.value
+
     # ---- device-resident step (benchmark) ---------------------------------
     def synthetic_inputs(self, seed: int = 0) -> None:
         N.check(N.LIB.hgnn_synthetic_inputs(self._h, seed))

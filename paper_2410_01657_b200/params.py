@@ -82,3 +82,37 @@ def mp_layer_slices(cfg: GnnConfig):
                 out.append((f"layer{m}.{which}.b{l}", off, off + H))
                 off += H
     return out
+
+
+def model_slices(cfg: "GnnConfig"):
+    """(name, start, stop) of every tensor of the full ModelParams::for_each
+    vector (model.cpp:124-135, nn.cpp:38-46): encoders (+ skip, ln_g, ln_b),
+    MP layers, decoder (+ skip)."""
+    H, k = cfg.hidden_dim, cfg.mlp_hidden_layers
+    out, off = [], 0
+
+    def mlp(prefix, in_dim, out_dim, skip, ln):
+        nonlocal off
+        for l in range(k + 2):
+            rows = in_dim if l == 0 else H
+            cols = out_dim if l == k + 1 else H
+            out.append((f"{prefix}.w{l}", off, off + rows * cols))
+            off += rows * cols
+            out.append((f"{prefix}.b{l}", off, off + cols))
+            off += cols
+        if skip:
+            out.append((f"{prefix}.skip", off, off + in_dim * out_dim))
+            off += in_dim * out_dim
+        if ln:
+            out.append((f"{prefix}.ln_g", off, off + out_dim))
+            off += out_dim
+            out.append((f"{prefix}.ln_b", off, off + out_dim))
+            off += out_dim
+
+    mlp("node_encoder", cfg.in_node_dim, H, True, True)
+    mlp("edge_encoder", cfg.in_edge_dim, H, True, True)
+    for m in range(cfg.num_mp_layers):
+        mlp(f"layer{m}.edge_update", 3 * H, H, False, False)
+        mlp(f"layer{m}.node_update", 2 * H, H, False, False)
+    mlp("node_decoder", H, cfg.out_dim, True, False)
+    return out
