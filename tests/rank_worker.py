@@ -41,7 +41,10 @@ def main():
     ap.add_argument("--k", type=int)
     ap.add_argument("--mode")
     ap.add_argument("--out")
+    ap.add_argument("--model", action="store_true", help="full model (encoders, loss, Adam) on TGV features")
     a = ap.parse_args()
+    if a.model:
+        return model_main(a)
     cfg = GnnConfig("w", a.H, a.M, a.k, mode=a.mode)
     g = build_rank_graph(a.E, a.p, a.R, a.rank, "verify")
     eng = Engine(a.rank, a.rank, a.R, bytes.fromhex(a.uid))
@@ -55,6 +58,24 @@ def main():
     x_out2 = eng.nmp_forward(x0, e0)
     np.savez(a.out, x_out=x_out, e_out=e_out, a_sync0=a_sync0, dx0=dx0, de0=de0, grads=grads, x_out2=x_out2,
              halo_bytes=eng.halo_bytes())
+    eng.close()
+
+
+def model_main(a):
+    """compute_gradients + 3 train steps on the reference's TGV features of this rank."""
+    import oracle as O
+    cfg = GnnConfig("w", a.H, a.M, a.k, mode=a.mode)
+    g = build_rank_graph(a.E, a.p, a.R, a.rank, "verify")
+    rg = O.RefGraph(a.E, a.p, a.R, "verify").ranks[a.rank]
+    eng = Engine(a.rank, a.rank, a.R, bytes.fromhex(a.uid))
+    eng.upload_graph(g)
+    eng.configure(cfg)
+    eng.model_configure(3, 7, 3)
+    eng.model_params_upload(O.ref_init_params(a.H, a.M, a.k, 11))
+    eng.model_set_data(rg.node_features, rg.edge_features, None)
+    loss, grads, y = eng.compute_gradients()
+    steps = [eng.train_step(lr=1e-3) for _ in range(3)]
+    np.savez(a.out, loss=loss, grads=grads, steps=np.array(steps), params=eng.model_params())
     eng.close()
 
 
