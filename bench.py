@@ -203,6 +203,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train-step", action="store_true")
     ap.add_argument("--ref-elements", type=int, default=5)
     ap.add_argument("--elements", type=int, default=0, help="override E (debug)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline / clocks")
@@ -310,6 +311,11 @@ def main():
     if not a.no_e2e and not a.profile:
         e2e = run_e2e(a, eng, g, cfg, stream, barrier, world, dist, torch, wl)
 
+    # ---- full training step on the device, supplementary
+    train = None
+    if not a.no_train_step and not a.profile:
+        train = run_train_step(a, eng, g, cfg, stream, barrier, world, dist, torch, wl)
+
     # ---- CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and n == 1 and not a.no_cpu_baseline and not a.profile:
@@ -325,7 +331,7 @@ def main():
                 "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic (seeded by global id; random-init weights init_params seed 0)",
                 "config": config_dict(wl, n), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
-                "cpu_baseline": cpu, "clocks": clk,
+                "cpu_baseline": cpu, "clocks": clk, "train_step": train,
                 "kernel_share": {c: round(v, 4) for c, v in step_share.items()},
                 "halo_share": round(step_share.get("halo", 0.0), 4), "halo_bytes_per_step_rank0": halo_bytes,
                 "graph_build_s": round(t_graph, 3),
@@ -334,6 +340,38 @@ def main():
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_train_step(a, eng, g, cfg, stream, barrier, world, dist, torch, wl, steps=2):
+    """hgnn_train_step (encoders + MP stack + decoder + consistent loss +
+    gradient AllReduce + Adam), device time per step, max over ranks.
+    Synthetic features of the reference shapes: F_x = 3, F_e = 7, autoencoding."""
+    from paper_2410_01657_b200 import init_params
+    eng.model_configure(3, 7, 3)
+    eng.model_params_upload(init_params(cfg, 0))
+    rng = np.random.default_rng(3)
+    node = np.sin(0.37 * g.global_ids[:, None] + np.arange(3)[None, :])
+    edge = rng.uniform(-1, 1, (g.num_edges, 7))
+    eng.model_set_data(node, edge, None)
+    eng.train_step()  # warm-up
+    barrier()
+    eng.kernel_timing(True)
+    k0 = eng.kernel_times()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    losses = [eng.train_step() for _ in range(steps)]
+    ev1.record(stream)
+    barrier()
+    k1 = eng.kernel_times()
+    eng.kernel_timing(False)
+    ms = ev0.elapsed_time(ev1) / steps
+    share = {c: round((k1[c][0] - k0[c][0]) / steps / ms, 4) for c in k1}
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"ms_per_step": ms, "unique_nodes_per_s": wl["unique_nodes"] / (ms / 1e3), "steps": steps,
+            "losses": losses, "kernel_share": share, "api": "hgnn_train_step (model.cpp:569-579 on the device)"}
 
 
 def run_e2e(a, eng, g, cfg, stream, barrier, world, dist, torch, wl):

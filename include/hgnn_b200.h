@@ -214,7 +214,8 @@ int hgnn_bench_alu(int kind, int iters, int threads, int blocks, uint64_t* cycle
  * events on its stream; totals are read back with hgnn_kernel_time. */
 enum {
   HGNN_K_EDGE_FWD = 0, HGNN_K_EDGE_BWD = 1, HGNN_K_NODE_FWD = 2, HGNN_K_NODE_BWD = 3,
-  HGNN_K_AGG = 4, HGNN_K_DX = 5, HGNN_K_HALO = 6, HGNN_K_GRAD_REDUCE = 7, HGNN_K_COUNT = 8
+  HGNN_K_AGG = 4, HGNN_K_DX = 5, HGNN_K_HALO = 6, HGNN_K_GRAD_REDUCE = 7,
+  HGNN_K_ENCODE = 8, HGNN_K_DECODE = 9, HGNN_K_LOSS_ADAM = 10, HGNN_K_COUNT = 11
 };
 int hgnn_kernel_timing(hgnn_ctx* ctx, int enable);
 int hgnn_kernel_time(hgnn_ctx* ctx, int kernel_class, double* total_ms, int64_t* launches);

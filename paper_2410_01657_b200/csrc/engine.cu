@@ -179,11 +179,14 @@ struct Timed {
     }
     CUDA_OK(cudaEventRecord(v[c->ev_used[cls]].a, c->stream));
   }
-  ~Timed() {
-    if (!c->timing) return;
+  ~Timed() { stop(); }
+  void stop() {
+    if (!c->timing || done) return;
+    done = true;
     cudaEventRecord(c->ev[cls][c->ev_used[cls]].b, c->stream);
     c->ev_used[cls] += 1;
   }
+  bool done = false;
 };
 
 // --------------------------------------------------------------------------
@@ -843,7 +846,7 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
   a.k = (int)c->K;
   a.n_par = n_par;
   auto k = gen_mlp_backward_kernel<IN, OUT, SKIP, LN, DIN>;
-  const size_t smem = (size_t)((n_par + 3) / 4) * 16 + (size_t)2 * kGenH * kGenThreads * 4;
+  const size_t smem = (size_t)((n_par + 3) / 4) * 16 + (size_t)2 * kGenThreads * kGenRow * 4;
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, kGenThreads, smem, c->stream>>>(a);
   check_launch(c);
@@ -864,15 +867,21 @@ void require_model(hgnn_ctx* c) {
 void model_compute_gradients(hgnn_ctx* c) {
   const int64_t H = c->H, nl = c->nl;
   ensure_buffers(c);
-  // encoders (model.cpp:289-294), every row / edge
-  gen_forward<3, 64, true, true>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
-  gen_forward<7, 64, true, true>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
+  {  // encoders (model.cpp:289-294), every row / edge
+    Timed t(c, HGNN_K_ENCODE);
+    gen_forward<3, 64, true, true>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
+    gen_forward<7, 64, true, true>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
+  }
   // message passing (model.cpp:295-300)
   run_forward(c);
   // decoder on local rows (model.cpp:303-306)
   c->y.alloc(std::max<int64_t>(nl * c->fy, 1));
   c->dy.alloc(std::max<int64_t>(nl * c->fy, 1));
-  gen_forward<64, 3, true, false>(c, nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
+  {
+    Timed t(c, HGNN_K_DECODE);
+    gen_forward<64, 3, true, false>(c, nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
+  }
+  Timed t_loss(c, HGNN_K_LOSS_ADAM);
   // consistent loss (model.cpp:455-480) and its adjoint (model.cpp:482-500)
   c->loss_part.alloc(2 * kLossBlocks);
   c->loss_st.alloc(3);
@@ -887,17 +896,22 @@ void model_compute_gradients(hgnn_ctx* c) {
   loss_backward_kernel<<<blocks_for(nl * c->fy), kEwThreads, 0, c->stream>>>(
       c->y.p, c->target.p, c->node_inv.p, c->loss_st.p + 2, nl, (int)c->fy, c->dy.p);
   check_launch(c);
-  // decoder backward (model.cpp:402-409): adjoint of x_M on local rows, halo rows 0
-  CUDA_OK(cudaMemsetAsync(c->dx.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
-  gen_backward<64, 3, true, false, true>(c, nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
+  t_loss.stop();
+  {  // decoder backward (model.cpp:402-409): adjoint of x_M on local rows, halo rows 0
+    Timed t(c, HGNN_K_DECODE);
+    CUDA_OK(cudaMemsetAsync(c->dx.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
+    gen_backward<64, 3, true, false, true>(c, nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
+  }
   // message-passing backward (model.cpp:411-415), de_M = 0 (model.cpp:412)
   CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * H), c->stream));
   run_backward(c);
   CUDA_OK(cudaMemcpyAsync(c->mgrads.p + c->off_mp, c->grads.p, sizeof(double) * (size_t)c->n_mp_par,
                           cudaMemcpyDeviceToDevice, c->stream));
-  // encoder backward (model.cpp:417-423)
-  gen_backward<3, 64, true, true, false>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
-  gen_backward<7, 64, true, true, false>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
+  {  // encoder backward (model.cpp:417-423)
+    Timed t(c, HGNN_K_ENCODE);
+    gen_backward<3, 64, true, true, false>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
+    gen_backward<7, 64, true, true, false>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
+  }
   // average over ranks (model.cpp:516-531)
   if (c->nranks > 1) {
     NCCL_OK(ncclAllReduce(c->mgrads.p, c->mgrads.p, (size_t)c->n_full, ncclDouble, ncclSum, c->comm, c->stream));
@@ -1532,6 +1546,7 @@ int hgnn_train_step(hgnn_ctx* c, double lr, double beta1, double beta2, double e
     c->adam_step += 1;
     const double bc1 = 1.0 - std::pow(beta1, (double)c->adam_step);
     const double bc2 = 1.0 - std::pow(beta2, (double)c->adam_step);
+    Timed t(c, HGNN_K_LOSS_ADAM);
     CUDA_OK(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), c->stream));
     adam_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->mgrads.p, c->adam_m.p,
                                                                      c->adam_v.p, c->n_full, lr, beta1, beta2, eps,
@@ -1542,6 +1557,7 @@ int hgnn_train_step(hgnn_ctx* c, double lr, double beta1, double beta2, double e
     CUDA_OK(cudaStreamSynchronize(c->stream));
     if (bad) fail(HGNN_ERR_OPTIMIZER, "adam_step: non-finite gradient");
     model_refresh_params(c);
+    t.stop();
     CUDA_OK(cudaStreamSynchronize(c->stream));
     if (loss) *loss = c->last_loss;
   });

@@ -27,6 +27,7 @@ namespace hgnn_b200 {
 
 constexpr int kGenThreads = 128;
 constexpr int kGenH = 64;
+constexpr int kGenRow = 68;  // staged row stride (floats): 16-byte aligned, conflict-free float4 row writes
 
 __host__ __device__ inline int64_t gen_param_count(int in_dim, int out_dim, int k, bool skip, bool out_ln) {
   const int H = kGenH;
@@ -65,20 +66,26 @@ struct GenArgs {
 
 __device__ __forceinline__ float gen_elu(float z) { return z > 0.f ? z : ptx::exp_fast(z) - 1.0f; }
 
+// Sum of N values with 4 independent chains.
+template <int N>
+__device__ __forceinline__ float gen_sum(const float (&v)[N]) {
+  float p[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < N; ++j) p[j % 4] += v[j];
+  return (p[0] + p[1]) + (p[2] + p[3]);
+}
+
 // Two-pass LayerNorm statistics of N values (kernels.cpp:81-94).
 template <int N>
 __device__ __forceinline__ void gen_ln_stats(const float (&v)[N], float& mean, float& inv_std) {
-  float s = 0.f;
-#pragma unroll
-  for (int j = 0; j < N; ++j) s += v[j];
-  mean = s * (1.0f / N);
-  float q = 0.f;
+  mean = gen_sum<N>(v) * (1.0f / N);
+  float q[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const float d = v[j] - mean;
-    q = fmaf(d, d, q);
+    q[j % 4] = fmaf(d, d, q[j % 4]);
   }
-  inv_std = ptx::rsqrt_fast(q * (1.0f / N) + 1e-12f);
+  inv_std = ptx::rsqrt_fast(((q[0] + q[1]) + (q[2] + q[3])) * (1.0f / N) + 1e-12f);
 }
 
 // acc[j] += sum_t v[t] W[t*NO + j] (W row-major, shared memory, warp-uniform reads)
@@ -104,27 +111,40 @@ __device__ __forceinline__ void gen_gemv(float (&acc)[NO], const float (&v)[NI],
   }
 }
 
-// acc[t] += sum_j d[j] W[t*NO + j]  (adjoint product d W^T)
+// acc[t] += sum_j d[j] W[t*NO + j]  (adjoint product d W^T). Eight outputs
+// at a time so eight independent FMA chains are in flight.
 template <int NI, int NO>
 __device__ __forceinline__ void gen_gemv_t(float (&acc)[NI], const float (&d)[NO], const float* __restrict__ W) {
 #pragma unroll
-  for (int t = 0; t < NI; ++t) {
-    float s = 0.f;
+  for (int t0 = 0; t0 < NI; t0 += 8) {
+    float s[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] = 0.f;
     if (NO % 4 == 0) {
-      const float4* w4 = reinterpret_cast<const float4*>(W + t * NO);
 #pragma unroll
       for (int j = 0; j < NO / 4; ++j) {
-        const float4 w = w4[j];
-        s = fmaf(d[4 * j], w.x, s);
-        s = fmaf(d[4 * j + 1], w.y, s);
-        s = fmaf(d[4 * j + 2], w.z, s);
-        s = fmaf(d[4 * j + 3], w.w, s);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (t0 + u < NI) {
+            const float4 w = reinterpret_cast<const float4*>(W + (t0 + u) * NO)[j];
+            s[u] = fmaf(d[4 * j], w.x, s[u]);
+            s[u] = fmaf(d[4 * j + 1], w.y, s[u]);
+            s[u] = fmaf(d[4 * j + 2], w.z, s[u]);
+            s[u] = fmaf(d[4 * j + 3], w.w, s[u]);
+          }
+        }
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < NO; ++j) s = fmaf(d[j], W[t * NO + j], s);
+      for (int j = 0; j < NO; ++j) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t0 + u < NI) s[u] = fmaf(d[j], W[(t0 + u) * NO + j], s[u]);
+      }
     }
-    acc[t] += s;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < NI) acc[t0 + u] += s[u];
   }
 }
 
@@ -198,33 +218,70 @@ __host__ __device__ inline int64_t gen_scratch_slots(int k, int out_dim) {
 
 // Tile reduction of dW += sum_rows A[r][i] D[r][j] for NI x NO, A / D staged
 // in shared memory as [i][row] / [j][row]; thread t owns elements t, t + T, ...
+// Tile reduction dW[i][j] += sum_rows A[r][i] D[r][j] (NI x NO), A / D staged
+// row-major ([row][kGenRow]). Each thread owns a 4 x BJ register block of dW
+// (i, j ascending, rows summed in order: deterministic) and reads it with
+// 16-byte shared loads: 3 loads per 32 FMAs.
 template <int NI, int NO>
 __device__ __forceinline__ void gen_dw_tile(float* __restrict__ gp, const float* __restrict__ sa,
                                             const float* __restrict__ sd) {
-  for (int e = threadIdx.x; e < NI * NO; e += kGenThreads) {
-    const int i = e / NO, j = e % NO;
-    const float* ar = sa + i * kGenThreads;
-    const float* dr = sd + j * kGenThreads;
-    float s = 0.f;
-#pragma unroll 8
-    for (int r = 0; r < kGenThreads; ++r) s = fmaf(ar[r], dr[r], s);
-    gp[e] += s;
+  constexpr int BJ = NO >= 8 ? 8 : 4;
+  constexpr int NBI = (NI + 3) / 4, NBJ = (NO + BJ - 1) / BJ;
+  for (int b = threadIdx.x; b < NBI * NBJ; b += kGenThreads) {
+    const int i0 = 4 * (b / NBJ), j0 = BJ * (b % NBJ);
+    float acc[4][BJ];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) acc[ii][jj] = 0.f;
+#pragma unroll 4
+    for (int r = 0; r < kGenThreads; ++r) {
+      const float4 av = *reinterpret_cast<const float4*>(sa + r * kGenRow + i0);
+      float dv[BJ];
+#pragma unroll
+      for (int q = 0; q < BJ / 4; ++q) {
+        const float4 t = *reinterpret_cast<const float4*>(sd + r * kGenRow + j0 + 4 * q);
+        dv[4 * q] = t.x;
+        dv[4 * q + 1] = t.y;
+        dv[4 * q + 2] = t.z;
+        dv[4 * q + 3] = t.w;
+      }
+      const float a4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) acc[ii][jj] = fmaf(a4[ii], dv[jj], acc[ii][jj]);
+    }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj)
+        if (i0 + ii < NI && j0 + jj < NO) gp[(i0 + ii) * NO + j0 + jj] += acc[ii][jj];
   }
 }
 template <int NO>
 __device__ __forceinline__ void gen_db_tile(float* __restrict__ gp, const float* __restrict__ sd) {
   for (int j = threadIdx.x; j < NO; j += kGenThreads) {
-    const float* dr = sd + j * kGenThreads;
-    float s = 0.f;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 8
-    for (int r = 0; r < kGenThreads; ++r) s += dr[r];
-    gp[j] += s;
+    for (int r = 0; r < kGenThreads; r += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] += sd[(r + u) * kGenRow + j];
+    }
+    gp[j] += (s[0] + s[1]) + (s[2] + s[3]);
   }
 }
+// This thread's row v[0..N) into the row-major staging buffer.
 template <int N>
 __device__ __forceinline__ void gen_stage_col(float* s, const float (&v)[N]) {
+  float* d = s + threadIdx.x * kGenRow;
+  if (N % 4 == 0) {
 #pragma unroll
-  for (int j = 0; j < N; ++j) s[j * kGenThreads + threadIdx.x] = v[j];
+    for (int j = 0; j < N; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) d[j] = v[j];
+  }
 }
 
 // smem: params | A stage (64 x T) | D stage (64 x T)
@@ -235,7 +292,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
   const GenLayout L{IN, OUT, a.k};
   const int K = a.k;
   float* sA = gsm + ((a.n_par + 3) / 4) * 4;
-  float* sD = sA + H * kGenThreads;
+  float* sD = sA + kGenThreads * kGenRow;
   gen_stage_params(gsm, a.params, a.n_par);
   float* gp = a.grad_partial + (int64_t)blockIdx.x * a.n_par;
   const int64_t slots = gen_scratch_slots(K, OUT);
@@ -352,16 +409,16 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
     // ---- hidden blocks in reverse (nn.cpp:259-274)
     for (int l = K; l >= 1; --l) {
       float du[H];
-      float gm = 0.f, gxm = 0.f;
+      float pm[4] = {0.f, 0.f, 0.f, 0.f}, px[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < H; ++j) {
         const float t = S(s_t + (int64_t)(l - 1) * H + j);
         du[j] = dh[j] * (t > 0.f ? 1.0f : ptx::exp_fast(t));  // elu', kernels.cpp:68-71
-        gm += du[j];
-        gxm = fmaf(du[j], t, gxm);
+        pm[j % 4] += du[j];
+        px[j % 4] = fmaf(du[j], t, px[j % 4]);
       }
-      gm *= 1.0f / H;
-      gxm *= 1.0f / H;
+      const float gm = ((pm[0] + pm[1]) + (pm[2] + pm[3])) * (1.0f / H);
+      const float gxm = ((px[0] + px[1]) + (px[2] + px[3])) * (1.0f / H);
       const float inv_std = S(s_inv + l - 1);
 #pragma unroll
       for (int j = 0; j < H; ++j) du[j] = (du[j] - gm - S(s_t + (int64_t)(l - 1) * H + j) * gxm) * inv_std;
