@@ -3,6 +3,9 @@
 //   mode 0: A in TMEM (TS), B K-major in SMEM          (forward / dX path)
 //   mode 1: A, B both MN-major in SMEM (SS), N = 128   (dW path)
 //   mode 2: A, B both K-major in SMEM (SS), N = 128
+//   modes 6-8: MN-major SWIZZLE_128B_BASE32B operands (dW path)
+//   modes 9/10: M = N = 64, both MN-major swizzled, D addressed at TMEM lane 0 / 16
+//               (D read back for all 128 lanes: where M = 64 rows land)
 // A: 128 x 32 (row-major m, k), B: 32 x N (row-major k, n), D = A B (fp32 out).
 #include <cstring>
 #include <vector>
@@ -43,17 +46,20 @@ __global__ void __launch_bounds__(128) selftest_kernel(int mode, const float* A,
   const int warp = t / 32;
   // stage operands
   const bool sw = mode >= 6;
-  const bool a_mn = mode == 1 || mode == 3 || mode == 5 || mode == 6 || mode == 7;
-  const bool b_mn = mode == 1 || mode == 4 || mode == 5 || mode == 6 || mode == 8;
+  const bool m64 = mode >= 9;  // M = N = 64, D at lane 0 (mode 9) or lane 64 (mode 10)
+  const bool a_mn = mode == 1 || mode == 3 || mode == 5 || mode == 6 || mode == 7 || m64;
+  const bool b_mn = mode == 1 || mode == 4 || mode == 5 || mode == 6 || mode == 8 || m64;
   // swizzled MN-major: MN atoms (128 B) at lbo = 512, K atoms (4 rows) at sbo = (MN/32) * 512
-  const uint32_t sw_lbo = 512, sw_sbo_a = (TM / 32) * 512, sw_sbo_b = (TN / 32) * 512;
+  const uint32_t sw_lbo = 512, sw_sbo_a = ((m64 ? 64 : TM) / 32) * 512, sw_sbo_b = ((m64 ? 64 : TN) / 32) * 512;
   for (int i = t; i < TM * TK; i += 128) {
     const int m = i / TK, k = i % TK;
+    if (m64 && m >= 64) continue;
     const uint32_t off = (sw && a_mn) ? mn_sw(m, k, sw_lbo, sw_sbo_a) : (a_mn ? mnmaj(m, k, TK) : kmaj(m, k, TM));
     *reinterpret_cast<float*>(sa + off) = A[i];
   }
   for (int i = t; i < TK * TN; i += 128) {
     const int k = i / TN, n = i % TN;
+    if (m64 && n >= 64) continue;
     const uint32_t off = (sw && b_mn) ? mn_sw(n, k, sw_lbo, sw_sbo_b) : (b_mn ? mnmaj(n, k, TK) : kmaj(n, k, TN));
     *reinterpret_cast<float*>(sb + off) = B[i];
   }
@@ -68,6 +74,12 @@ __global__ void __launch_bounds__(128) selftest_kernel(int mode, const float* A,
   ptx::tc_fence_after();
   const uint32_t tmem = tslot;
   const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+  if (m64) {  // zero D region (all lanes, columns [0, 128)) so untouched lanes read back as 0
+    float z[32];
+    for (int j = 0; j < 32; ++j) z[j] = 0.f;
+    for (int c = 0; c < 128; c += 32) ptx::tmem_st32(tmem + lane_off + c, z);
+    ptx::tmem_wait_st();
+  }
   if (mode == 0) {  // A into TMEM columns [128, 160): thread = row
     float v[32];
     for (int k = 0; k < 32; ++k) v[k] = A[t * TK + k];
@@ -86,7 +98,7 @@ __global__ void __launch_bounds__(128) selftest_kernel(int mode, const float* A,
         ptx::mma_tf32_ts(tmem, tmem + 128 + 8 * ks, bd, ptx::idesc_tf32(128, TN), ks > 0);
       } else {
         uint64_t ad, bd;
-        uint32_t idesc = ptx::idesc_tf32(128, TN);
+        uint32_t idesc = m64 ? ptx::idesc_tf32(64, 64) : ptx::idesc_tf32(128, TN);
         const uint32_t lbo_a = (TM / 8) * 128, lbo_b = (TN / 8) * 128;
         const uint32_t mn_lbo = mode == 5 ? (TK / 8) * 128 : 128, mn_sbo = mode == 5 ? 128 : (TK / 8) * 128;
         ad = a_mn ? ptx::smem_desc(a_s + ks * 128, mn_lbo, mn_sbo) : ptx::smem_desc(a_s + ks * 2 * lbo_a, lbo_a, 128);
@@ -100,7 +112,7 @@ __global__ void __launch_bounds__(128) selftest_kernel(int mode, const float* A,
         if (b_mn) idesc |= (1u << 16);
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (mode == 10 ? (16u << 16) : 0u)),
             "l"(ad), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1u : 0u)
             : "memory");
       }
