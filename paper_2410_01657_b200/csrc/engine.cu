@@ -830,7 +830,7 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
     return;
   }
   const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->num_sms));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));  // 2 CTAs / SM
   const int64_t slots = gen_scratch_slots((int)c->K, OUT);
   c->gen_part.alloc(std::max<int64_t>(c->gen_part.n, (int64_t)grid * n_par));
   c->gen_scratch.alloc(std::max<int64_t>(c->gen_scratch.n, (int64_t)grid * slots * kGenThreads));
@@ -846,7 +846,7 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
   a.k = (int)c->K;
   a.n_par = n_par;
   auto k = gen_mlp_backward_kernel<IN, OUT, SKIP, LN, DIN>;
-  const size_t smem = (size_t)((n_par + 3) / 4) * 16 + (size_t)2 * kGenThreads * kGenRow * 4;
+  const size_t smem = gen_backward_smem(IN, OUT);
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, kGenThreads, smem, c->stream>>>(a);
   check_launch(c);

@@ -212,6 +212,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a)
 // ------------------------------------------------------------------ backward
 // Scratch slots per row: hidden states h_0..h_k (k+1) x H, normed t_1..t_k
 // k x H, inv_std k, pre-LayerNorm output OUT (+ mean / inv_std 2).
+// Dynamic shared memory of gen_mlp_backward_kernel<IN, OUT, ...>.
+__host__ __device__ inline size_t gen_backward_smem(int in_dim, int out_dim) {
+  const int H = kGenH;
+  const int wblk = (H * H + H) > (in_dim * H + H) ? (H * H + H) : (in_dim * H + H);
+  return (size_t)(((wblk + 3) / 4) * 4 + ((in_dim * out_dim + 3) / 4) * 4 + ((out_dim + 3) / 4) * 4 +
+                  2 * kGenThreads * kGenRow) * 4;
+}
+
 __host__ __device__ inline int64_t gen_scratch_slots(int k, int out_dim) {
   return (int64_t)(2 * k + 1) * kGenH + k + out_dim + 2;
 }
@@ -284,16 +292,34 @@ __device__ __forceinline__ void gen_stage_col(float* s, const float (&v)[N]) {
   }
 }
 
-// smem: params | A stage (64 x T) | D stage (64 x T)
+// smem: one streamed layer block (W, b) | skip weights | LN gamma | A stage | D stage.
+// Weights are streamed layer by layer (the CTA walks the layers of its tile in
+// lock-step), so two CTAs fit per SM.
 template <int IN, int OUT, bool SKIP, bool OUT_LN, bool DIN>
 __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a) {
   constexpr int H = kGenH;
   extern __shared__ __align__(16) float gsm[];
   const GenLayout L{IN, OUT, a.k};
   const int K = a.k;
-  float* sA = gsm + ((a.n_par + 3) / 4) * 4;
+  constexpr int WBLK = ((H * H + H) > (IN * H + H) ? (H * H + H) : (IN * H + H));
+  constexpr int SW_N = ((WBLK + 3) / 4) * 4, SK_N = ((IN * OUT + 3) / 4) * 4, LN_N = ((OUT + 3) / 4) * 4;
+  float* sW = gsm;
+  float* sSkip = sW + SW_N;
+  float* sG = sSkip + SK_N;
+  float* sA = sG + LN_N;
   float* sD = sA + kGenThreads * kGenRow;
-  gen_stage_params(gsm, a.params, a.n_par);
+  if (SKIP)
+    for (int i = threadIdx.x; i < IN * OUT; i += kGenThreads) sSkip[i] = __ldg(a.params + L.skip() + i);
+  if (OUT_LN)
+    for (int i = threadIdx.x; i < OUT; i += kGenThreads) sG[i] = __ldg(a.params + L.ln_g() + i);
+  // (W, b) of linear l into sW; all threads of the CTA call it together
+  auto load_linear = [&](int l) -> const float* {
+    const int rows = l == 0 ? IN : H, cols = l == K + 1 ? OUT : H;
+    __syncthreads();
+    gen_stage_params(sW, a.params + L.w(l), (int64_t)rows * cols + cols);
+    __syncthreads();
+    return sW;
+  };
   float* gp = a.grad_partial + (int64_t)blockIdx.x * a.n_par;
   const int64_t slots = gen_scratch_slots(K, OUT);
   float* scr = a.scratch + (int64_t)blockIdx.x * slots * kGenThreads + threadIdx.x;
@@ -310,17 +336,19 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       {
         float x[IN];
         gen_load_row<IN>(x, a.in + row * IN, valid);
+        const float* W = load_linear(0);
 #pragma unroll
-        for (int j = 0; j < H; ++j) h[j] = gsm[L.b(0) + j];
-        gen_gemv<IN, H>(h, x, gsm + L.w(0));
+        for (int j = 0; j < H; ++j) h[j] = W[IN * H + j];
+        gen_gemv<IN, H>(h, x, W);
       }
 #pragma unroll
       for (int j = 0; j < H; ++j) S(s_h + j) = h[j];
       for (int l = 1; l <= K; ++l) {
         float u[H];
+        const float* W = load_linear(l);
 #pragma unroll
-        for (int j = 0; j < H; ++j) u[j] = gsm[L.b(l) + j];
-        gen_gemv<H, H>(u, h, gsm + L.w(l));
+        for (int j = 0; j < H; ++j) u[j] = W[H * H + j];
+        gen_gemv<H, H>(u, h, W);
         float mean, inv_std;
         gen_ln_stats<H>(u, mean, inv_std);
 #pragma unroll
@@ -333,13 +361,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
         S(s_inv + l - 1) = inv_std;
       }
       float y[OUT];
+      const float* W = load_linear(K + 1);
 #pragma unroll
-      for (int j = 0; j < OUT; ++j) y[j] = gsm[L.b(K + 1) + j];
-      gen_gemv<H, OUT>(y, h, gsm + L.w(K + 1));
+      for (int j = 0; j < OUT; ++j) y[j] = W[H * OUT + j];
+      gen_gemv<H, OUT>(y, h, W);
       if (SKIP) {
         float x[IN];
         gen_load_row<IN>(x, a.in + row * IN, valid);
-        gen_gemv<IN, OUT>(y, x, gsm + L.skip());
+        gen_gemv<IN, OUT>(y, x, sSkip);
       }
       if (OUT_LN) {
         float mean, inv_std;
@@ -360,7 +389,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       float gdy[OUT], gm = 0.f, gxm = 0.f;
 #pragma unroll
       for (int j = 0; j < OUT; ++j) {
-        gdy[j] = gsm[L.ln_g() + j] * dy[j];
+        gdy[j] = sG[j] * dy[j];
         gm += gdy[j];
         gxm = fmaf(gdy[j], xh[j], gxm);
       }
@@ -403,7 +432,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       }
 #pragma unroll
       for (int j = 0; j < H; ++j) dh[j] = 0.f;
-      gen_gemv_t<H, OUT>(dh, dy, gsm + L.w(K + 1));
+      gen_gemv_t<H, OUT>(dh, dy, load_linear(K + 1));
     }
 
     // ---- hidden blocks in reverse (nn.cpp:259-274)
@@ -433,10 +462,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       }
       gen_dw_tile<H, H>(gp + L.w(l), sA, sD);
       gen_db_tile<H>(gp + L.b(l), sD);
-      gen_gemv_t<H, H>(dh, du, gsm + L.w(l));  // d_prev = d_u W^T + d_h
+      gen_gemv_t<H, H>(dh, du, load_linear(l));  // d_prev = d_u W^T + d_h
     }
     // ---- input projection (nn.cpp:277-281)
     if (DIN) {  // d_in = d_h W0^T (+ d_y W_skip^T), 16 input columns at a time
+      const float* W0 = load_linear(0);
 #pragma unroll
       for (int c = 0; c < IN; c += 16) {
         float din[16];
@@ -444,11 +474,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
         for (int t = 0; t < 16; ++t) {
           float s = 0.f;
           if (c + t < IN) {
-            const float* w0 = gsm + L.w(0) + (int64_t)(c + t) * H;
+            const float* w0 = W0 + (int64_t)(c + t) * H;
 #pragma unroll
             for (int j = 0; j < H; ++j) s = fmaf(dh[j], w0[j], s);
             if (SKIP) {
-              const float* ws = gsm + L.skip() + (int64_t)(c + t) * OUT;
+              const float* ws = sSkip + (int64_t)(c + t) * OUT;
 #pragma unroll
               for (int j = 0; j < OUT; ++j) s = fmaf(dy[j], ws[j], s);
             }
