@@ -589,56 +589,29 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         }
       };
       unsigned long long pc_fwd = 0, pc_mma = 0;  // phase cycles (profiling only)
+      // One loop over the linears of a tile (single inlined copy of the MMA
+      // sequence keeps the issuer's code small): forward recompute (input
+      // segments, hidden blocks), backward output linear and hidden blocks in
+      // reverse (D pre-loaded with the residual d_h except for the output
+      // linear), backward input segments. dW MMAs run on the dW issuer.
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
         const long long t_p0 = PROF ? clock64() : 0;
-        // forward recompute: input chunks then hidden blocks (no output linear)
-        for (int c = 0; c < nseg; ++c) {
+#pragma unroll 1
+        for (int st = 0; st < n_w; ++st) {
+          const bool first_zero = st == 0 || (st >= nseg && st < nseg + K) || st >= nseg + 2 * K + 1 ||
+                                  st == nseg + K;  // recompute input c = 0, recompute hidden, input dX, output dX
+          const bool to_a_empty = st + 1 < nseg;   // recompute input segments before the last
+          if (PROF && st == nseg + K) pc_fwd += (unsigned long long)(clock64() - t_p0);
           const uint32_t bb = next_w();
-          for (int s = 0; s < 2; ++s) {
-            timed_wait(&a_full[s], pa[s], pc_a);
-            pa[s] ^= 1;
-            ptx::tc_fence_after();
-            mma3(s, bb, c == 0);
-            ptx::mma_commit_w(c + 1 < nseg ? &a_empty[s] : &d_full[s]);
-          }
-          release_w();
-        }
-        for (int l = 1; l <= K; ++l) {
-          const uint32_t bb = next_w();
-          for (int s = 0; s < 2; ++s) {
-            timed_wait(&a_full[s], pa[s], pc_a);
-            pa[s] ^= 1;
-            ptx::tc_fence_after();
-            mma3(s, bb, true);
-            ptx::mma_commit_w(&d_full[s]);
-          }
-          release_w();
-        }
-        if (PROF) pc_fwd += (unsigned long long)(clock64() - t_p0);
-        // backward: output linear, hidden blocks in reverse (dX then dW each);
-        // hidden steps accumulate onto D pre-loaded with the residual d_h
-        for (int step = 0; step <= K; ++step) {
-          const uint32_t bb = next_w();
+#pragma unroll 1
           for (int s = 0; s < 2; ++s) {
             timed_wait(&a_full[s], pa[s], pc_a);
             pa[s] ^= 1;
             ptx::tc_fence_after();
             const long long t_m0 = PROF ? clock64() : 0;
-            mma3(s, bb, step == 0);
-            ptx::mma_commit_w(&d_full[s]);
+            mma3(s, bb, first_zero);
+            ptx::mma_commit_w(to_a_empty ? &a_empty[s] : &d_full[s]);
             if (PROF) pc_mma += (unsigned long long)(clock64() - t_m0);
-          }
-          release_w();
-        }
-        // input linear: per segment, dX (dW on the dW issuer)
-        for (int c = 0; c < nseg; ++c) {
-          const uint32_t bb = next_w();
-          for (int s = 0; s < 2; ++s) {
-            timed_wait(&a_full[s], pa[s], pc_a);
-            pa[s] ^= 1;
-            ptx::tc_fence_after();
-            mma3(s, bb, true);
-            ptx::mma_commit_w(&d_full[s]);
           }
           release_w();
         }
