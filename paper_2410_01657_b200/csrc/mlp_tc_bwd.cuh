@@ -453,86 +453,86 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
 #pragma unroll
         for (int j = 0; j < H; ++j) dh[j] = 0.f;
       }
-      // output projection (nn.cpp:241-245): dX = d_y W_out^T, dW_out += h_k^T d_y
-      bwd_store_a(t_ahi, t_alo, dh);
-      tc_signal(&a_full[g]);
-      write_db(dh);
-      stage_chunk(h, dh);
-      wait_dx();
-      ++job;
-      bwd_load_d(t_d, nullptr, dh);
-      // residual blocks in reverse (nn.cpp:259-274)
-      for (int l = K; l >= 1; --l) {
-        const float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
-        const float inv_std = scr_inv[(l - 1) * 128 + trow];
-        const long long tl0 = PROF ? clock64() : 0;
-        bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
-        float p1[8], p2[8];
+      // One loop over the tile's backward linears (a single inlined copy of the
+      // staging / drain / column-sum code keeps the kernel's instruction
+      // footprint small): jb = 0 output linear (nn.cpp:241-245), jb = 1..K
+      // residual blocks in reverse (nn.cpp:259-274), jb = K+1.. input segments
+      // (nn.cpp:277-281). Every job: dX = d W^T on the tensor cores, dW += h^T d.
+      long long ti0 = 0;
+#pragma unroll 1
+      for (int jb = 0; jb < K + 1 + nseg; ++jb) {
+        const int c = jb - (K + 1);  // input segment (>= 0 in the input phase)
+        if (jb >= 1 && jb <= K) {
+          const int l = K + 1 - jb;
+          const float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
+          const float inv_std = scr_inv[(l - 1) * 128 + trow];
+          const long long tl0 = PROF ? clock64() : 0;
+          bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
+          float p1[8], p2[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
+          for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float4 t4 = ptx::ld_hint(st + q * 128, keep);
-          const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+          for (int q = 0; q < 16; ++q) {
+            const float4 t4 = ptx::ld_hint(st + q * 128, keep);
+            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = 4 * q + u;
-            const float t = tv[u];
-            const float ex = ptx::exp_fast(t);
-            const float elu = t > 0.f ? t : ex - 1.0f;
-            const float dd = dh[j] * (t > 0.f ? 1.0f : ex);  // elu', kernels.cpp:68-71
-            h[j] -= elu;                                     // h_{l-1}
-            dh[j] = dd;
-            p1[j % 8] += dd;
-            p2[j % 8] = fmaf(dd, t, p2[j % 8]);
+            for (int u = 0; u < 4; ++u) {
+              const int jx = 4 * q + u;
+              const float t = tv[u];
+              const float ex = ptx::exp_fast(t);
+              const float elu = t > 0.f ? t : ex - 1.0f;
+              const float dd = dh[jx] * (t > 0.f ? 1.0f : ex);  // elu', kernels.cpp:68-71
+              h[jx] -= elu;                                      // h_{l-1}
+              dh[jx] = dd;
+              p1[jx % 8] += dd;
+              p2[jx % 8] = fmaf(dd, t, p2[jx % 8]);
+            }
           }
-        }
-        const float g_mean = (((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]))) * (1.0f / H);
-        const float gx_mean =
-            (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
+          const float g_mean =
+              (((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]))) * (1.0f / H);
+          const float gx_mean =
+              (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float4 t4 = ptx::ld_hint(st + q * 128, keep);
-          dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
-          dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
-          dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
-          dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
+          for (int q = 0; q < 16; ++q) {
+            const float4 t4 = ptx::ld_hint(st + q * 128, keep);
+            dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
+            dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
+            dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
+            dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
+          }
+          if (PROF) pf[6] += (unsigned long long)(clock64() - tl0);
         }
-        if (PROF) pf[6] += (unsigned long long)(clock64() - tl0);
-        bwd_store_a(t_ahi, t_alo, dh);
-        tc_signal(&a_full[g]);
-        write_db(dh);
+        if (c == 0 && PROF) ti0 = clock64();
+        if (c <= 0) {  // new A operand (split d) for this linear; the input segments share one
+          bwd_store_a(t_ahi, t_alo, dh);
+          tc_signal(&a_full[g]);
+          write_db(dh);
+        }
+        if (c >= 0) bwd_gather<MODE>(a, row, valid, c, h);  // dW0 segment operand
         stage_chunk(h, dh);
         wait_dx();
         ++job;
-        bwd_load_d(t_d, nullptr, dh);  // d_prev = d_u W^T + d_h
-      }
-      const long long ti0 = PROF ? clock64() : 0;
-      // input projection (nn.cpp:277-281): per segment c, dW0[seg c] and d_in[seg c]
-      bwd_store_a(t_ahi, t_alo, dh);
-      tc_signal(&a_full[g]);
-      write_db(dh);
-      for (int c = 0; c < nseg; ++c) {
-        bwd_gather<MODE>(a, row, valid, c, h);
-        stage_chunk(h, dh);
-        wait_dx();
-        ++job;
-        float* outp;
-        if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
-        else outp = c == 0 ? a.d_a_out : a.d_x_out;
-        float4* o = reinterpret_cast<float4*>(outp + row * H);
+        if (c < 0) {
+          bwd_load_d(t_d, nullptr, dh);  // d_prev = d_u W^T + d_h
+        } else {
+          float* outp;
+          if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
+          else outp = c == 0 ? a.d_a_out : a.d_x_out;
+          float4* o = reinterpret_cast<float4*>(outp + row * H);
 #pragma unroll
-        for (int cc = 0; cc < H; cc += 16) {
-          float p[16];
-          ptx::tmem_ld16(t_d + cc, p);
-          ptx::tmem_wait_ld();
-          if (valid) {
+          for (int cc = 0; cc < H; cc += 16) {
+            float p[16];
+            ptx::tmem_ld16(t_d + cc, p);
+            ptx::tmem_wait_ld();
+            if (valid) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              ptx::st_hint(o + cc / 4 + j, make_float4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]), once);
+              for (int jx = 0; jx < 4; ++jx)
+                ptx::st_hint(o + cc / 4 + jx, make_float4(p[4 * jx], p[4 * jx + 1], p[4 * jx + 2], p[4 * jx + 3]),
+                             once);
+            }
           }
+          if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays
         }
-        if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays
       }
       if (PROF) pf[7] += (unsigned long long)(clock64() - ti0);
     }
