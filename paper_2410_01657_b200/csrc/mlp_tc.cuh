@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       float h[H];
       const long long t_in0 = PROF ? clock64() : 0;
       // input projection: nseg K-chunks streamed through A, next one prefetched
+#pragma unroll 1
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
           const long long t0 = PROF ? clock64() : 0;

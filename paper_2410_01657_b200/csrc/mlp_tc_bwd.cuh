@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       float h[H];
       const long long tr0 = PROF ? clock64() : 0;
       // ---------------------------------------------- forward recompute
+#pragma unroll 1
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
           ptx::mbar_wait(&a_empty[g], pe);

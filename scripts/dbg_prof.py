@@ -2,7 +2,7 @@ import sys, numpy as np, time
 sys.path.insert(0, "/root/repo")
 from paper_2410_01657_b200 import Engine, GnnConfig, build_rank_graph, init_params, mp_params, _native as N
 H, M, k = 64, 1, 5
-for E in (8,):
+for E in ((int(sys.argv[1]),) if len(sys.argv) > 1 else (8,)):
     cfg = GnnConfig("p", H, M, k, mode="na2a")
     g = build_rank_graph(E, 5, 1, 0)
     eng = Engine(0); eng.upload_graph(g); eng.configure(cfg); eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
