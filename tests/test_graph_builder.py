@@ -123,3 +123,17 @@ def test_partition_errors():
         build_rank_graph(4, 2, 8, 0, "block", (3, 1, 1))
     assert balanced_factors(8, 4) == (2, 2, 2)
     assert balanced_factors(4, 50) == (2, 2, 1)
+
+
+def test_model_slices_cover_the_full_parameter_vector():
+    """model_slices (encoders, MP layers, decoder; nn.cpp:38-46 names) tile
+    the full ModelParams::for_each vector exactly (model.cpp:124-135)."""
+    from paper_2410_01657_b200 import GnnConfig, model_slices, param_count
+    for H, M, k in ((64, 4, 5), (64, 2, 2), (32, 3, 1)):
+        cfg = GnnConfig("s", H, M, k)
+        sl = model_slices(cfg)
+        assert sl[0][1] == 0 and sl[-1][2] == param_count(cfg)
+        assert all(a[2] == b[1] for a, b in zip(sl, sl[1:]))
+        names = [n for n, _, _ in sl]
+        assert names[0] == "node_encoder.w0" and names[-1] == "node_decoder.skip"
+        assert "edge_encoder.ln_b" in names and f"layer{M - 1}.node_update.b{k + 1}" in names
