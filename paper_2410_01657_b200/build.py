@@ -29,8 +29,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-Xcompiler", "-Wall"]
 
-SOURCES = ["engine.cu", "selftest.cu", "host_graph.cpp", "host_params.cpp"]
-HEADERS = ["common.hpp", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh"]
+SOURCES = ["engine.cu", "model.cu", "selftest.cu", "host_graph.cpp", "host_params.cpp"]
+HEADERS = ["common.hpp", "engine_ctx.hpp", "mlp_generic.cuh", "model_kernels.cuh", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh"]
 
 
 def _newer(src: list[Path], out: Path) -> bool:

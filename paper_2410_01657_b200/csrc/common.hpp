@@ -11,6 +11,8 @@
 
 namespace hgnn_b200 {
 
+constexpr int kEwThreads = 256;  // block size of the element-wise kernels
+
 struct Error : std::runtime_error {
   int code;
   Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}

@@ -9,8 +9,6 @@
 //   dx, dxn, d_a        node adjoints;  de, dsrc, ddst  edge adjoints (N_e x H)
 // Edge slot p = position in the reference in-CSR (graph.cpp:122-136); the
 // boundary permutes to / from the reference edge-id order.
-#include <nccl.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -18,176 +16,29 @@
 #include <string>
 #include <vector>
 
-#include "common.hpp"
+#include "engine_ctx.hpp"
 #include "graph_kernels.cuh"
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
 #include "mlp_tc_bwd.cuh"
-#include "mlp_generic.cuh"
-#include "model_kernels.cuh"
 
 using namespace hgnn_b200;
+using namespace hgnn_b200::engine;
 
-#define CUDA_OK(expr)                                                                                  \
-  do {                                                                                                 \
-    cudaError_t _e = (expr);                                                                           \
-    if (_e != cudaSuccess) fail(HGNN_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));    \
-  } while (0)
-#define NCCL_OK(expr)                                                                                  \
-  do {                                                                                                 \
-    ncclResult_t _r = (expr);                                                                          \
-    if (_r != ncclSuccess) fail(HGNN_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));    \
-  } while (0)
 
-namespace {
-
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  int64_t n = 0;
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() { release(); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  void alloc(int64_t count) {
-    if (count == n && p) return;
-    release();
-    if (count <= 0) return;
-    CUDA_OK(cudaMalloc(&p, sizeof(T) * (size_t)count));
-    n = count;
-  }
-  void upload(const T* h, int64_t count, cudaStream_t s) {
-    alloc(count);
-    if (count > 0) CUDA_OK(cudaMemcpyAsync(p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, s));
-  }
-};
-
-struct EventPair {
-  cudaEvent_t a, b;
-};
-
-}  // namespace
-
-struct hgnn_ctx {
-  int device = 0;
-  int32_t rank = 0, nranks = 1;
-  cudaStream_t stream = nullptr;
-  ncclComm_t comm = nullptr;
-  int num_sms = 148;
-
-  // configuration
-  int64_t H = 0, M = 0, K = 0;
-  int mode = HGNN_MODE_NONE;
-  bool configured = false, graph_ready = false, params_ready = false, forward_done = false;
-
-  // graph
-  int64_t nl = 0, nh = 0, rows = 0, ne = 0, max_buffer_rows = 0;
-  DevBuf<int32_t> src, dst, in_off, twin, slot_of;
-  DevBuf<float> inv;
-  DevBuf<int64_t> gid;
-  // halo
-  std::vector<int32_t> h_nbr, h_send_off, h_recv_off;
-  std::vector<int64_t> h_recv_base;
-  DevBuf<int32_t> send_rows, recv_rows, sync_local, sync_off, sync_slots, acc_rows, acc_off;
-  DevBuf<int64_t> pos_na2a, pos_a2a_send, pos_a2a_recv, acc_pos_na2a, acc_pos_a2a;
-  int64_t n_send = 0, n_recv = 0, n_sync = 0, n_acc = 0;
-  DevBuf<float> sendbuf, recvbuf;
-
-  // parameters (fp32) and gradients (fp64), MP layers
-  int64_t n_edge_par = 0, n_node_par = 0, n_mp_par = 0;
-  DevBuf<float> par, par_t;
-  DevBuf<float> chunks;                 // tcgen05 B operands, [W_hi | W_lo]^T chunks per MLP
-  std::vector<int64_t> chunk_off;       // per (layer, edge/node)
-  DevBuf<double> grads;
-  int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
-  int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
-  DevBuf<float> bchunks;                // backward chunk sequence per MLP
-  std::vector<int64_t> bchunk_off;
-  DevBuf<float> tc_scratch;
-  DevBuf<unsigned long long> prof;      // optional backward-kernel wait profile
-  bool prof_on = false;
-
-  // activations
-  std::vector<std::unique_ptr<DevBuf<float>>> xs, es, as;
-  DevBuf<float> dx, dxn, d_a, de, dsrc, ddst, dx_in;
-  DevBuf<float> grad_part, scratch;
-  DevBuf<double> stage;
-  int64_t stage_elems = 0;
-
-  // MLP launch geometry
-  int grid_edge_f = 0, grid_edge_b = 0, grid_node_f = 0, grid_node_b = 0;
-  size_t smem_edge_f = 0, smem_edge_b = 0, smem_node_f = 0, smem_node_b = 0;
-  bool wsm_edge_f = false, wsm_edge_b = false, wsm_node_f = false, wsm_node_b = false;
-
-  // model level: encoders, decoder, consistent loss,
-  // gradient averaging, Adam. Parameters: full ModelParams::for_each vector.
-  DevBuf<double> node_inv;                         // [num_local] 1/d per local node (loss weights)
-  int64_t fx = 0, fe = 0, fy = 0;
-  bool model_configured = false, model_params_ready = false, model_data_ready = false;
-  int64_t off_ne = 0, off_ee = 0, off_mp = 0, off_dec = 0, n_ne = 0, n_ee = 0, n_dec = 0, n_full = 0;
-  DevBuf<double> mparams, mgrads, adam_m, adam_v;  // fp64 master parameters, gradients, Adam moments
-  DevBuf<float> gen_par;                           // fp32 copy of the full vector (encoders / decoder read it)
-  DevBuf<float> node_feat, edge_feat, target, y, dy;
-  DevBuf<float> gen_part, gen_scratch;
-  DevBuf<double> loss_part, loss_st;               // block partials; [s, n, seed]
-  DevBuf<int32_t> pt_src;                          // par_t[i] = par[pt_src[i]] (MP block)
-  DevBuf<uint32_t> ch_map, bch_map;                // chunk refresh maps (bit 31: tf32 lo part)
-  DevBuf<int> nonfinite;
-  int64_t adam_step = 0;
-  double last_loss = 0.0;
-
-  // instrumentation
-  bool timing = false;
-  std::vector<EventPair> ev[HGNN_K_COUNT];
-  size_t ev_used[HGNN_K_COUNT] = {};
-  int64_t launches = 0;
-  int64_t halo_bytes = 0;
-};
-
-namespace {
+namespace hgnn_b200::engine {
 
 void bind(hgnn_ctx* c) {
   if (!c) fail(HGNN_ERR_CONFIG, "null hgnn_ctx");
   CUDA_OK(cudaSetDevice(c->device));
 }
 
-inline unsigned blocks_for(int64_t n, int threads = kEwThreads) {
-  return (unsigned)std::max<int64_t>(1, (n + threads - 1) / threads);
-}
 
 void check_launch(hgnn_ctx* c) {
   c->launches += 1;
   CUDA_OK(cudaGetLastError());
 }
 
-struct Timed {
-  hgnn_ctx* c;
-  int cls;
-  Timed(hgnn_ctx* ctx, int k) : c(ctx), cls(k) {
-    if (!c->timing) return;
-    auto& v = c->ev[cls];
-    if (c->ev_used[cls] == v.size()) {
-      EventPair p;
-      CUDA_OK(cudaEventCreate(&p.a));
-      CUDA_OK(cudaEventCreate(&p.b));
-      v.push_back(p);
-    }
-    CUDA_OK(cudaEventRecord(v[c->ev_used[cls]].a, c->stream));
-  }
-  ~Timed() { stop(); }
-  void stop() {
-    if (!c->timing || done) return;
-    done = true;
-    cudaEventRecord(c->ev[cls][c->ev_used[cls]].b, c->stream);
-    c->ev_used[cls] += 1;
-  }
-  bool done = false;
-};
 
 // --------------------------------------------------------------------------
 // MLP kernel dispatch over the supported hidden widths
@@ -274,49 +125,6 @@ bool tc_eligible(const hgnn_ctx* c) { return c->H == 32 || c->H == 64; }
 // Chunks of one processor MLP in MMA order: the input linear split into
 // nseg K-chunks of H rows, then one chunk per H x H linear. Each chunk is the
 // B operand [W_hi | W_lo]^T (2H x H) in K-major core-matrix order.
-// Chunk layouts of one MLP's tcgen05 B operands. emit(pos, src, lo) places
-// element `src` of the MLP's for_each parameter block at chunk float `pos`,
-// as its tf32 hi part (lo = false) or lo part (lo = true).
-// Forward sequence (mlp_tc.cuh): input segments of W0, W1 .. W_{k+1}.
-template <class Emit>
-void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
-  const int nseg = in_dim / H;
-  for (int l = 0; l < K + 2; ++l) {
-    const int64_t w = mlp_w_offset(l, in_dim, H);
-    const int n_ch = l == 0 ? nseg : 1;
-    for (int cidx = 0; cidx < n_ch; ++cidx, base += 2 * (int64_t)H * H)
-      for (int kk = 0; kk < H; ++kk)
-        for (int n = 0; n < H; ++n) {
-          const int64_t src = w + (int64_t)(cidx * H + kk) * H + n;
-          emit(base + tc_chunk_index(n, kk, H), src, false);
-          emit(base + tc_chunk_index(H + n, kk, H), src, true);
-        }
-  }
-}
-// Backward sequence (mlp_tc_bwd.cuh): the forward chunks of the recompute
-// (input segments, hidden linears), then W_{k+1}^T, W_k^T .. W_1^T and W_0^T
-// per input segment. A transposed chunk stores element (n = input feature,
-// k = output feature) = W[n][k].
-template <class Emit>
-void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
-  const int nseg = in_dim / H;
-  auto chunk = [&](auto src_of) {
-    for (int kk = 0; kk < H; ++kk)
-      for (int n = 0; n < H; ++n) {
-        const int64_t src = src_of(n, kk);
-        emit(base + tc_chunk_index(n, kk, H), src, false);
-        emit(base + tc_chunk_index(H + n, kk, H), src, true);
-      }
-    base += 2 * (int64_t)H * H;
-  };
-  auto W = [&](int l) { return mlp_w_offset(l, in_dim, H); };
-  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + kk) * H + n; });
-  for (int l = 1; l <= K; ++l) chunk([&](int n, int kk) { return W(l) + (int64_t)kk * H + n; });
-  for (int l = K + 1; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * H + kk; });
-  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + n) * H + kk; });
-}
-int64_t chunk_floats_fwd(int in_dim, int H, int K) { return (int64_t)(in_dim / H + K + 1) * 2 * H * H; }
-int64_t chunk_floats_bwd(int in_dim, int H, int K) { return (int64_t)(2 * (in_dim / H) + 2 * K + 1) * 2 * H * H; }
 
 void build_chunks(const float* p, int in_dim, int H, int K, std::vector<float>& out) {
   const int64_t base = (int64_t)out.size();
@@ -402,6 +210,16 @@ void rows_to_host(hgnn_ctx* c, const float* d, int64_t n, double* h) {
     CUDA_OK(cudaMemcpyAsync(h + o, c->stage.p, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
   }
   CUDA_OK(cudaStreamSynchronize(c->stream));
+}
+void edges_cols_to_device(hgnn_ctx* c, const double* h, int cols, float* d) {
+  const int64_t per = std::max<int64_t>(1, c->stage_elems / cols);
+  for (int64_t e0 = 0; e0 < c->ne; e0 += per) {
+    const int64_t m = std::min(per, c->ne - e0);
+    CUDA_OK(cudaMemcpyAsync(c->stage.p, h + e0 * cols, sizeof(double) * (size_t)(m * cols), cudaMemcpyHostToDevice,
+                            c->stream));
+    edges_in_kernel<<<blocks_for(m * cols), kEwThreads, 0, c->stream>>>(c->stage.p, c->slot_of.p, e0, m, cols, d);
+    check_launch(c);
+  }
 }
 void edges_to_device(hgnn_ctx* c, const double* h, float* d) {
   const int64_t H = c->H, per = std::max<int64_t>(1, c->stage_elems / H);
@@ -544,11 +362,8 @@ void launch_tc_typed(hgnn_ctx* c, const TcFwdArgs& args) {
   using Cfg = TcCfg<H>;
   const bool prof = args.prof != nullptr;
   auto k = prof ? mlp_tc_forward_kernel<H, MODE, true> : mlp_tc_forward_kernel<H, MODE, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[prof]) {
-    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
-    attr[prof] = true;
-  }
+  // per launch: the attribute belongs to the current device (cheap host call)
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
   const int64_t pairs = ((args.n_rows + 127) / 128 + 1) / 2;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
   k<<<grid, Cfg::THREADS, Cfg::SMEM, c->stream>>>(args);
@@ -600,11 +415,7 @@ int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
   const bool prof = args.prof != nullptr;
   auto k = edge ? (prof ? mlp_tc_backward_kernel<kEdgeInput, true> : mlp_tc_backward_kernel<kEdgeInput, false>)
                 : (prof ? mlp_tc_backward_kernel<kNodeInput, true> : mlp_tc_backward_kernel<kNodeInput, false>);
-  static bool attr[2][2] = {{false, false}, {false, false}};
-  if (!attr[edge][prof]) {
-    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
-    attr[edge][prof] = true;
-  }
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
   k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(args);
   check_launch(c);
   return grid;
@@ -789,207 +600,8 @@ void require_ready(hgnn_ctx* c) {
     fail(HGNN_ERR_CONFIG, "nmp_layer: exchange mode requires a rank runtime");
 }
 
-}  // namespace
+}  // namespace hgnn_b200::engine
 
-
-// ==========================================================================
-// model level: encoders + MP stack + decoder, consistent loss, gradient
-// averaging, Adam (model.cpp:289-307, 390-424, 455-579,
-// nn.cpp:331-360)
-// ==========================================================================
-namespace {
-
-bool gen_supported(int64_t fx, int64_t fe, int64_t fy) { return fx == 3 && fe == 7 && fy == 3; }
-
-template <int IN, int OUT, bool SKIP, bool LN>
-void gen_forward(hgnn_ctx* c, int64_t n_rows, const float* in, float* out, int64_t par_off, int64_t n_par) {
-  if (n_rows == 0) return;
-  GenArgs a{};
-  a.n_rows = n_rows;
-  a.in = in;
-  a.out = out;
-  a.params = c->gen_par.p + par_off;
-  a.k = (int)c->K;
-  a.n_par = n_par;
-  auto k = gen_mlp_forward_kernel<IN, OUT, SKIP, LN>;
-  const size_t smem = (size_t)n_par * 4;
-  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));
-  k<<<grid, kGenThreads, smem, c->stream>>>(a);
-  check_launch(c);
-}
-
-// Backward of one encoder / decoder MLP; parameter gradients (rank-local)
-// land in mgrads[par_off, par_off + n_par).
-template <int IN, int OUT, bool SKIP, bool LN, bool DIN>
-void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_out, float* d_in, int64_t par_off,
-                  int64_t n_par) {
-  if (n_rows == 0) {
-    CUDA_OK(cudaMemsetAsync(c->mgrads.p + par_off, 0, sizeof(double) * (size_t)n_par, c->stream));
-    return;
-  }
-  const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));  // 2 CTAs / SM
-  const int64_t slots = gen_scratch_slots((int)c->K, OUT);
-  c->gen_part.alloc(std::max<int64_t>(c->gen_part.n, (int64_t)grid * n_par));
-  c->gen_scratch.alloc(std::max<int64_t>(c->gen_scratch.n, (int64_t)grid * slots * kGenThreads));
-  CUDA_OK(cudaMemsetAsync(c->gen_part.p, 0, sizeof(float) * (size_t)(grid * n_par), c->stream));
-  GenArgs a{};
-  a.n_rows = n_rows;
-  a.in = in;
-  a.d_out = d_out;
-  a.d_in = d_in;
-  a.params = c->gen_par.p + par_off;
-  a.grad_partial = c->gen_part.p;
-  a.scratch = c->gen_scratch.p;
-  a.k = (int)c->K;
-  a.n_par = n_par;
-  auto k = gen_mlp_backward_kernel<IN, OUT, SKIP, LN, DIN>;
-  const size_t smem = gen_backward_smem(IN, OUT);
-  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<grid, kGenThreads, smem, c->stream>>>(a);
-  check_launch(c);
-  reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->gen_part.p, grid, n_par,
-                                                                          c->mgrads.p + par_off);
-  check_launch(c);
-}
-
-void require_model(hgnn_ctx* c) {
-  require_ready(c);
-  if (!c->model_configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_configure has not been called");
-  if (!c->model_params_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_params_upload has not been called");
-  if (!c->model_data_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_set_data has not been called");
-}
-
-// compute_gradients (model.cpp:556-567) on the device; rank-averaged
-// gradients in mgrads, loss in c->last_loss.
-void model_compute_gradients(hgnn_ctx* c) {
-  const int64_t H = c->H, nl = c->nl;
-  ensure_buffers(c);
-  {  // encoders (model.cpp:289-294), every row / edge
-    Timed t(c, HGNN_K_ENCODE);
-    gen_forward<3, 64, true, true>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
-    gen_forward<7, 64, true, true>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
-  }
-  // message passing (model.cpp:295-300)
-  run_forward(c);
-  // decoder on local rows (model.cpp:303-306)
-  c->y.alloc(std::max<int64_t>(nl * c->fy, 1));
-  c->dy.alloc(std::max<int64_t>(nl * c->fy, 1));
-  {
-    Timed t(c, HGNN_K_DECODE);
-    gen_forward<64, 3, true, false>(c, nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
-  }
-  Timed t_loss(c, HGNN_K_LOSS_ADAM);
-  // consistent loss (model.cpp:455-480) and its adjoint (model.cpp:482-500)
-  c->loss_part.alloc(2 * kLossBlocks);
-  c->loss_st.alloc(3);
-  loss_partial_kernel<<<kLossBlocks, kLossThreads, 0, c->stream>>>(c->y.p, c->target.p, c->node_inv.p, nl,
-                                                                   (int)c->fy, c->loss_part.p);
-  check_launch(c);
-  loss_final_kernel<<<1, 32, 0, c->stream>>>(c->loss_part.p, kLossBlocks, c->loss_st.p);
-  check_launch(c);
-  if (c->nranks > 1) NCCL_OK(ncclAllReduce(c->loss_st.p, c->loss_st.p, 2, ncclDouble, ncclSum, c->comm, c->stream));
-  loss_seed_kernel<<<1, 32, 0, c->stream>>>(c->loss_st.p, (int)c->fy, c->nranks);
-  check_launch(c);
-  loss_backward_kernel<<<blocks_for(nl * c->fy), kEwThreads, 0, c->stream>>>(
-      c->y.p, c->target.p, c->node_inv.p, c->loss_st.p + 2, nl, (int)c->fy, c->dy.p);
-  check_launch(c);
-  t_loss.stop();
-  {  // decoder backward (model.cpp:402-409): adjoint of x_M on local rows, halo rows 0
-    Timed t(c, HGNN_K_DECODE);
-    CUDA_OK(cudaMemsetAsync(c->dx.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
-    gen_backward<64, 3, true, false, true>(c, nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
-  }
-  // message-passing backward (model.cpp:411-415), de_M = 0 (model.cpp:412)
-  CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * H), c->stream));
-  run_backward(c);
-  CUDA_OK(cudaMemcpyAsync(c->mgrads.p + c->off_mp, c->grads.p, sizeof(double) * (size_t)c->n_mp_par,
-                          cudaMemcpyDeviceToDevice, c->stream));
-  {  // encoder backward (model.cpp:417-423)
-    Timed t(c, HGNN_K_ENCODE);
-    gen_backward<3, 64, true, true, false>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
-    gen_backward<7, 64, true, true, false>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
-  }
-  // average over ranks (model.cpp:516-531)
-  if (c->nranks > 1) {
-    NCCL_OK(ncclAllReduce(c->mgrads.p, c->mgrads.p, (size_t)c->n_full, ncclDouble, ncclSum, c->comm, c->stream));
-    scale_f64_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mgrads.p, c->n_full,
-                                                                           1.0 / (double)c->nranks);
-    check_launch(c);
-  }
-  double st[2];
-  CUDA_OK(cudaMemcpyAsync(st, c->loss_st.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));
-  c->last_loss = st[0] / (st[1] * (double)c->fy);
-}
-
-// fp32 / tf32 images of the parameters from the fp64 master copy.
-void model_refresh_params(hgnn_ctx* c) {
-  f64_to_f32_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->n_full, c->gen_par.p);
-  check_launch(c);
-  const double* mp = c->mparams.p + c->off_mp;
-  f64_to_f32_kernel<<<blocks_for(c->n_mp_par), kEwThreads, 0, c->stream>>>(mp, c->n_mp_par, c->par.p);
-  check_launch(c);
-  gather_f64_to_f32_kernel<<<blocks_for(c->n_mp_par), kEwThreads, 0, c->stream>>>(mp, c->pt_src.p, c->n_mp_par,
-                                                                                  c->par_t.p);
-  check_launch(c);
-  if (c->ch_map.n > 0) {
-    chunk_refresh_kernel<<<blocks_for(c->ch_map.n), kEwThreads, 0, c->stream>>>(mp, c->ch_map.p, c->ch_map.n,
-                                                                              c->chunks.p);
-    check_launch(c);
-  }
-  if (c->bch_map.n > 0) {
-    chunk_refresh_kernel<<<blocks_for(c->bch_map.n), kEwThreads, 0, c->stream>>>(mp, c->bch_map.p, c->bch_map.n,
-                                                                                c->bchunks.p);
-    check_launch(c);
-  }
-}
-
-// Device-refresh maps of the MP block (same element placement as the host
-// builders in hgnn_params_upload).
-void build_refresh_maps(hgnn_ctx* c) {
-  const int H = (int)c->H, K = (int)c->K;
-  std::vector<int32_t> pt((size_t)c->n_mp_par);
-  std::vector<uint32_t> ch, bch;
-  int64_t off = 0;
-  for (int64_t m = 0; m < c->M; ++m)
-    for (int which = 0; which < 2; ++which) {
-      const int in_dim = (which == 0 ? 3 : 2) * H;
-      for (int l = 0; l < K + 2; ++l) {
-        const int rin = l == 0 ? in_dim : H;
-        const int64_t wo = off + mlp_w_offset(l, in_dim, H), bo = off + mlp_b_offset(l, in_dim, H);
-        for (int i = 0; i < rin; ++i)
-          for (int j = 0; j < H; ++j) pt[(size_t)(wo + (int64_t)j * rin + i)] = (int32_t)(wo + (int64_t)i * H + j);
-        for (int j = 0; j < H; ++j) pt[(size_t)(bo + j)] = (int32_t)(bo + j);
-      }
-      if (tc_eligible(c)) {
-        const int64_t base = (int64_t)ch.size();
-        ch.resize((size_t)(base + chunk_floats_fwd(in_dim, H, K)));
-        chunk_layout_fwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
-          ch[(size_t)pos] = (uint32_t)(off + src) | (lo ? 0x80000000u : 0u);
-        });
-      }
-      if (H == 64) {
-        const int64_t base = (int64_t)bch.size();
-        bch.resize((size_t)(base + chunk_floats_bwd(in_dim, H, K)));
-        chunk_layout_bwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
-          bch[(size_t)pos] = (uint32_t)(off + src) | (lo ? 0x80000000u : 0u);
-        });
-      }
-      off += mlp_param_count(in_dim, H, K);
-    }
-  c->pt_src.upload(pt.data(), (int64_t)pt.size(), c->stream);
-  c->ch_map.upload(ch.data(), (int64_t)ch.size(), c->stream);
-  c->bch_map.upload(bch.data(), (int64_t)bch.size(), c->stream);
-}
-
-}  // namespace
-
-// ==========================================================================
-// C-ABI
-// ==========================================================================
 extern "C" {
 
 int hgnn_device_count(void) {
@@ -1430,137 +1042,6 @@ int64_t hgnn_halo_bytes(hgnn_ctx* c, int reset) {
   const int64_t n = c->halo_bytes;
   if (reset) c->halo_bytes = 0;
   return n;
-}
-
-// ---- model level ----------------------------------------
-int hgnn_model_configure(hgnn_ctx* c, int64_t in_node_dim, int64_t in_edge_dim, int64_t out_dim) {
-  return guarded([&] {
-    bind(c);
-    if (!c->configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_configure has not been called");
-    if (c->H != kGenH) fail(HGNN_ERR_CONFIG, "model level: hidden width 64 only");
-    if (!gen_supported(in_node_dim, in_edge_dim, out_dim))
-      fail(HGNN_ERR_CONFIG, "model level: feature widths (F_x, F_e, F_y) = (3, 7, 3) supported");
-    c->fx = in_node_dim;
-    c->fe = in_edge_dim;
-    c->fy = out_dim;
-    const int K = (int)c->K;
-    c->n_ne = gen_param_count((int)c->fx, kGenH, K, true, true);
-    c->n_ee = gen_param_count((int)c->fe, kGenH, K, true, true);
-    c->n_dec = gen_param_count(kGenH, (int)c->fy, K, true, false);
-    c->off_ne = 0;
-    c->off_ee = c->n_ne;
-    c->off_mp = c->off_ee + c->n_ee;
-    c->off_dec = c->off_mp + c->n_mp_par;
-    c->n_full = c->off_dec + c->n_dec;
-    c->model_configured = true;
-    c->model_params_ready = c->model_data_ready = false;
-  });
-}
-
-int64_t hgnn_model_param_count(hgnn_ctx* c) { return c && c->model_configured ? c->n_full : -1; }
-
-int hgnn_model_params_upload(hgnn_ctx* c, const double* params, int64_t count) {
-  return guarded([&] {
-    bind(c);
-    if (!c->model_configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_configure has not been called");
-    if (count != c->n_full)
-      fail(HGNN_ERR_SHAPE, "hgnn_model_params_upload: expected " + std::to_string(c->n_full) + " values");
-    const int rc = hgnn_params_upload(c, params + c->off_mp, c->n_mp_par);
-    if (rc != HGNN_OK) fail(rc, hgnn_last_error());
-    c->mparams.upload(params, count, c->stream);
-    c->mgrads.alloc(count);
-    c->adam_m.alloc(count);
-    c->adam_v.alloc(count);
-    CUDA_OK(cudaMemsetAsync(c->adam_m.p, 0, sizeof(double) * (size_t)count, c->stream));
-    CUDA_OK(cudaMemsetAsync(c->adam_v.p, 0, sizeof(double) * (size_t)count, c->stream));
-    c->adam_step = 0;
-    c->gen_par.alloc(count);
-    f64_to_f32_kernel<<<blocks_for(count), kEwThreads, 0, c->stream>>>(c->mparams.p, count, c->gen_par.p);
-    check_launch(c);
-    build_refresh_maps(c);
-    c->nonfinite.alloc(1);
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    c->model_params_ready = true;
-  });
-}
-
-int hgnn_model_params_download(hgnn_ctx* c, double* params) {
-  return guarded([&] {
-    bind(c);
-    if (!c->model_params_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_params_upload has not been called");
-    CUDA_OK(cudaMemcpy(params, c->mparams.p, sizeof(double) * (size_t)c->n_full, cudaMemcpyDeviceToHost));
-  });
-}
-
-int hgnn_model_set_data(hgnn_ctx* c, const double* node_features, const double* edge_features,
-                        const double* target) {
-  return guarded([&] {
-    bind(c);
-    require_ready(c);
-    if (!c->model_configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_configure has not been called");
-    if (!node_features || !edge_features) fail(HGNN_ERR_SHAPE, "hgnn_model_set_data: null features");
-    if (!c->node_inv.p && c->nl > 0)
-      fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_set_data: the graph was uploaded without node_inv_degree");
-    ensure_buffers(c);
-    c->node_feat.alloc(std::max<int64_t>(c->rows * c->fx, 1));
-    rows_to_device(c, node_features, c->rows * c->fx, c->node_feat.p);
-    c->edge_feat.alloc(std::max<int64_t>(c->ne * c->fe, 1));
-    const int64_t per = std::max<int64_t>(1, c->stage_elems / c->fe);
-    for (int64_t e0 = 0; e0 < c->ne; e0 += per) {  // reference edge-id order -> receiver-sorted slots
-      const int64_t m = std::min(per, c->ne - e0);
-      CUDA_OK(cudaMemcpyAsync(c->stage.p, edge_features + e0 * c->fe, sizeof(double) * (size_t)(m * c->fe),
-                              cudaMemcpyHostToDevice, c->stream));
-      edges_in_kernel<<<blocks_for(m * c->fe), kEwThreads, 0, c->stream>>>(c->stage.p, c->slot_of.p, e0, m,
-                                                                          (int)c->fe, c->edge_feat.p);
-      check_launch(c);
-    }
-    c->target.alloc(std::max<int64_t>(c->nl * c->fy, 1));
-    if (target) {
-      rows_to_device(c, target, c->nl * c->fy, c->target.p);
-    } else {  // autoencoding (model.cpp:605-607): target = local rows of the node features
-      if (c->fy != c->fx) fail(HGNN_ERR_SHAPE, "autoencoding target needs out_dim == in_node_dim");
-      CUDA_OK(cudaMemcpyAsync(c->target.p, c->node_feat.p, sizeof(float) * (size_t)(c->nl * c->fy),
-                              cudaMemcpyDeviceToDevice, c->stream));
-    }
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    c->model_data_ready = true;
-  });
-}
-
-int hgnn_compute_gradients(hgnn_ctx* c, double* loss, double* grads, double* y) {
-  return guarded([&] {
-    bind(c);
-    require_model(c);
-    model_compute_gradients(c);
-    if (loss) *loss = c->last_loss;
-    if (grads) CUDA_OK(cudaMemcpy(grads, c->mgrads.p, sizeof(double) * (size_t)c->n_full, cudaMemcpyDeviceToHost));
-    if (y) rows_to_host(c, c->y.p, c->nl * c->fy, y);
-  });
-}
-
-int hgnn_train_step(hgnn_ctx* c, double lr, double beta1, double beta2, double eps, double* loss) {
-  return guarded([&] {
-    bind(c);
-    require_model(c);
-    model_compute_gradients(c);
-    c->adam_step += 1;
-    const double bc1 = 1.0 - std::pow(beta1, (double)c->adam_step);
-    const double bc2 = 1.0 - std::pow(beta2, (double)c->adam_step);
-    Timed t(c, HGNN_K_LOSS_ADAM);
-    CUDA_OK(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), c->stream));
-    adam_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->mgrads.p, c->adam_m.p,
-                                                                     c->adam_v.p, c->n_full, lr, beta1, beta2, eps,
-                                                                     bc1, bc2, c->nonfinite.p);
-    check_launch(c);
-    int bad = 0;
-    CUDA_OK(cudaMemcpyAsync(&bad, c->nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    if (bad) fail(HGNN_ERR_OPTIMIZER, "adam_step: non-finite gradient");
-    model_refresh_params(c);
-    t.stop();
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    if (loss) *loss = c->last_loss;
-  });
 }
 
 }  // extern "C"

@@ -1,0 +1,228 @@
+// Internal state of the device engine shared by engine.cu (message-passing
+// stack, C-ABI) and model.cu (encoders, decoder, loss, Adam): the per-rank
+// context, device buffers, error macros and the engine helpers model.cu uses.
+#pragma once
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "mlp_simt.cuh"
+#include "mlp_tc.cuh"
+
+#define CUDA_OK(expr)                                                                                  \
+  do {                                                                                                 \
+    cudaError_t _e = (expr);                                                                           \
+    if (_e != cudaSuccess) fail(HGNN_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+  } while (0)
+#define NCCL_OK(expr)                                                                                  \
+  do {                                                                                                 \
+    ncclResult_t _r = (expr);                                                                          \
+    if (_r != ncclSuccess) fail(HGNN_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));    \
+  } while (0)
+
+namespace hgnn_b200 {
+
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(int64_t count) {
+    if (count == n && p) return;
+    release();
+    if (count <= 0) return;
+    CUDA_OK(cudaMalloc(&p, sizeof(T) * (size_t)count));
+    n = count;
+  }
+  void upload(const T* h, int64_t count, cudaStream_t s) {
+    alloc(count);
+    if (count > 0) CUDA_OK(cudaMemcpyAsync(p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, s));
+  }
+};
+
+struct EventPair {
+  cudaEvent_t a, b;
+};
+
+
+}  // namespace hgnn_b200
+
+struct hgnn_ctx {
+  int device = 0;
+  int32_t rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+
+  // configuration
+  int64_t H = 0, M = 0, K = 0;
+  int mode = HGNN_MODE_NONE;
+  bool configured = false, graph_ready = false, params_ready = false, forward_done = false;
+
+  // graph
+  int64_t nl = 0, nh = 0, rows = 0, ne = 0, max_buffer_rows = 0;
+  hgnn_b200::DevBuf<int32_t> src, dst, in_off, twin, slot_of;
+  hgnn_b200::DevBuf<float> inv;
+  hgnn_b200::DevBuf<int64_t> gid;
+  // halo
+  std::vector<int32_t> h_nbr, h_send_off, h_recv_off;
+  std::vector<int64_t> h_recv_base;
+  hgnn_b200::DevBuf<int32_t> send_rows, recv_rows, sync_local, sync_off, sync_slots, acc_rows, acc_off;
+  hgnn_b200::DevBuf<int64_t> pos_na2a, pos_a2a_send, pos_a2a_recv, acc_pos_na2a, acc_pos_a2a;
+  int64_t n_send = 0, n_recv = 0, n_sync = 0, n_acc = 0;
+  hgnn_b200::DevBuf<float> sendbuf, recvbuf;
+
+  // parameters (fp32) and gradients (fp64), MP layers
+  int64_t n_edge_par = 0, n_node_par = 0, n_mp_par = 0;
+  hgnn_b200::DevBuf<float> par, par_t;
+  hgnn_b200::DevBuf<float> chunks;                 // tcgen05 B operands, [W_hi | W_lo]^T chunks per MLP
+  std::vector<int64_t> chunk_off;       // per (layer, edge/node)
+  hgnn_b200::DevBuf<double> grads;
+  int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
+  int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
+  hgnn_b200::DevBuf<float> bchunks;                // backward chunk sequence per MLP
+  std::vector<int64_t> bchunk_off;
+  hgnn_b200::DevBuf<float> tc_scratch;
+  hgnn_b200::DevBuf<unsigned long long> prof;      // optional backward-kernel wait profile
+  bool prof_on = false;
+
+  // activations
+  std::vector<std::unique_ptr<hgnn_b200::DevBuf<float>>> xs, es, as;
+  hgnn_b200::DevBuf<float> dx, dxn, d_a, de, dsrc, ddst, dx_in;
+  hgnn_b200::DevBuf<float> grad_part, scratch;
+  hgnn_b200::DevBuf<double> stage;
+  int64_t stage_elems = 0;
+
+  // MLP launch geometry
+  int grid_edge_f = 0, grid_edge_b = 0, grid_node_f = 0, grid_node_b = 0;
+  size_t smem_edge_f = 0, smem_edge_b = 0, smem_node_f = 0, smem_node_b = 0;
+  bool wsm_edge_f = false, wsm_edge_b = false, wsm_node_f = false, wsm_node_b = false;
+
+  // model level: encoders, decoder, consistent loss,
+  // gradient averaging, Adam. Parameters: full ModelParams::for_each vector.
+  hgnn_b200::DevBuf<double> node_inv;                         // [num_local] 1/d per local node (loss weights)
+  int64_t fx = 0, fe = 0, fy = 0;
+  bool model_configured = false, model_params_ready = false, model_data_ready = false;
+  int64_t off_ne = 0, off_ee = 0, off_mp = 0, off_dec = 0, n_ne = 0, n_ee = 0, n_dec = 0, n_full = 0;
+  hgnn_b200::DevBuf<double> mparams, mgrads, adam_m, adam_v;  // fp64 master parameters, gradients, Adam moments
+  hgnn_b200::DevBuf<float> gen_par;                           // fp32 copy of the full vector (encoders / decoder read it)
+  hgnn_b200::DevBuf<float> node_feat, edge_feat, target, y, dy;
+  hgnn_b200::DevBuf<float> gen_part, gen_scratch;
+  hgnn_b200::DevBuf<double> loss_part, loss_st;               // block partials; [s, n, seed]
+  hgnn_b200::DevBuf<int32_t> pt_src;                          // par_t[i] = par[pt_src[i]] (MP block)
+  hgnn_b200::DevBuf<uint32_t> ch_map, bch_map;                // chunk refresh maps (bit 31: tf32 lo part)
+  hgnn_b200::DevBuf<int> nonfinite;
+  int64_t adam_step = 0;
+  double last_loss = 0.0;
+
+  // instrumentation
+  bool timing = false;
+  std::vector<hgnn_b200::EventPair> ev[HGNN_K_COUNT];
+  size_t ev_used[HGNN_K_COUNT] = {};
+  int64_t launches = 0;
+  int64_t halo_bytes = 0;
+};
+
+namespace hgnn_b200::engine {
+
+inline unsigned blocks_for(int64_t n, int threads = kEwThreads) {
+  return (unsigned)std::max<int64_t>(1, (n + threads - 1) / threads);
+}
+
+
+struct Timed {
+  hgnn_ctx* c;
+  int cls;
+  Timed(hgnn_ctx* ctx, int k) : c(ctx), cls(k) {
+    if (!c->timing) return;
+    auto& v = c->ev[cls];
+    if (c->ev_used[cls] == v.size()) {
+      EventPair p;
+      CUDA_OK(cudaEventCreate(&p.a));
+      CUDA_OK(cudaEventCreate(&p.b));
+      v.push_back(p);
+    }
+    CUDA_OK(cudaEventRecord(v[c->ev_used[cls]].a, c->stream));
+  }
+  ~Timed() { stop(); }
+  void stop() {
+    if (!c->timing || done) return;
+    done = true;
+    cudaEventRecord(c->ev[cls][c->ev_used[cls]].b, c->stream);
+    c->ev_used[cls] += 1;
+  }
+  bool done = false;
+};
+
+// Chunk layouts of one MLP's tcgen05 B operands. emit(pos, src, lo) places
+// element `src` of the MLP's for_each parameter block at chunk float `pos`,
+// as its tf32 hi part (lo = false) or lo part (lo = true).
+// Forward sequence (mlp_tc.cuh): input segments of W0, W1 .. W_{k+1}.
+template <class Emit>
+void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
+  const int nseg = in_dim / H;
+  for (int l = 0; l < K + 2; ++l) {
+    const int64_t w = mlp_w_offset(l, in_dim, H);
+    const int n_ch = l == 0 ? nseg : 1;
+    for (int cidx = 0; cidx < n_ch; ++cidx, base += 2 * (int64_t)H * H)
+      for (int kk = 0; kk < H; ++kk)
+        for (int n = 0; n < H; ++n) {
+          const int64_t src = w + (int64_t)(cidx * H + kk) * H + n;
+          emit(base + tc_chunk_index(n, kk, H), src, false);
+          emit(base + tc_chunk_index(H + n, kk, H), src, true);
+        }
+  }
+}
+// Backward sequence (mlp_tc_bwd.cuh): the forward chunks of the recompute
+// (input segments, hidden linears), then W_{k+1}^T, W_k^T .. W_1^T and W_0^T
+// per input segment. A transposed chunk stores element (n = input feature,
+// k = output feature) = W[n][k].
+template <class Emit>
+void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
+  const int nseg = in_dim / H;
+  auto chunk = [&](auto src_of) {
+    for (int kk = 0; kk < H; ++kk)
+      for (int n = 0; n < H; ++n) {
+        const int64_t src = src_of(n, kk);
+        emit(base + tc_chunk_index(n, kk, H), src, false);
+        emit(base + tc_chunk_index(H + n, kk, H), src, true);
+      }
+    base += 2 * (int64_t)H * H;
+  };
+  auto W = [&](int l) { return mlp_w_offset(l, in_dim, H); };
+  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + kk) * H + n; });
+  for (int l = 1; l <= K; ++l) chunk([&](int n, int kk) { return W(l) + (int64_t)kk * H + n; });
+  for (int l = K + 1; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * H + kk; });
+  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + n) * H + kk; });
+}
+inline int64_t chunk_floats_fwd(int in_dim, int H, int K) { return (int64_t)(in_dim / H + K + 1) * 2 * H * H; }
+inline int64_t chunk_floats_bwd(int in_dim, int H, int K) { return (int64_t)(2 * (in_dim / H) + 2 * K + 1) * 2 * H * H; }
+
+void bind(hgnn_ctx* c);
+void check_launch(hgnn_ctx* c);
+bool tc_eligible(const hgnn_ctx* c);
+void ensure_buffers(hgnn_ctx* c);
+void require_ready(hgnn_ctx* c);
+void run_forward(hgnn_ctx* c);
+void run_backward(hgnn_ctx* c);
+// fp64 host rows -> fp32 device (n values), and back (synchronous)
+void rows_to_device(hgnn_ctx* c, const double* h, int64_t n, float* d);
+void rows_to_host(hgnn_ctx* c, const float* d, int64_t n, double* h);
+// N_e x cols fp64 host rows in reference edge-id order -> fp32 receiver-sorted slots
+void edges_cols_to_device(hgnn_ctx* c, const double* h, int cols, float* d);
+
+}  // namespace hgnn_b200::engine

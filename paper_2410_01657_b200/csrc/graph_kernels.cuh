@@ -12,9 +12,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-namespace hgnn_b200 {
+#include "common.hpp"
 
-constexpr int kEwThreads = 256;
+namespace hgnn_b200 {
 
 __device__ __forceinline__ float4 f4_fma(float s, float4 v, float4 acc) {
   return make_float4(fmaf(s, v.x, acc.x), fmaf(s, v.y, acc.y), fmaf(s, v.z, acc.z), fmaf(s, v.w, acc.w));

@@ -1,0 +1,329 @@
+// Model level on the device: encoders + MP stack +
+// decoder, consistent loss, rank-averaged gradients, Adam (model.cpp:289-307,
+// 390-424, 455-579; nn.cpp:331-360) and their C-ABI (include/hgnn_b200.h).
+#include <cmath>
+
+#include "engine_ctx.hpp"
+#include "mlp_generic.cuh"
+#include "model_kernels.cuh"
+
+using namespace hgnn_b200;
+using namespace hgnn_b200::engine;
+
+namespace {
+
+bool gen_supported(int64_t fx, int64_t fe, int64_t fy) { return fx == 3 && fe == 7 && fy == 3; }
+
+template <int IN, int OUT, bool SKIP, bool LN>
+void gen_forward(hgnn_ctx* c, int64_t n_rows, const float* in, float* out, int64_t par_off, int64_t n_par) {
+  if (n_rows == 0) return;
+  GenArgs a{};
+  a.n_rows = n_rows;
+  a.in = in;
+  a.out = out;
+  a.params = c->gen_par.p + par_off;
+  a.k = (int)c->K;
+  a.n_par = n_par;
+  auto k = gen_mlp_forward_kernel<IN, OUT, SKIP, LN>;
+  const size_t smem = (size_t)n_par * 4;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));
+  k<<<grid, kGenThreads, smem, c->stream>>>(a);
+  check_launch(c);
+}
+
+// Backward of one encoder / decoder MLP; parameter gradients (rank-local)
+// land in mgrads[par_off, par_off + n_par).
+template <int IN, int OUT, bool SKIP, bool LN, bool DIN>
+void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_out, float* d_in, int64_t par_off,
+                  int64_t n_par) {
+  if (n_rows == 0) {
+    CUDA_OK(cudaMemsetAsync(c->mgrads.p + par_off, 0, sizeof(double) * (size_t)n_par, c->stream));
+    return;
+  }
+  const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));  // 2 CTAs / SM
+  const int64_t slots = gen_scratch_slots((int)c->K, OUT);
+  c->gen_part.alloc(std::max<int64_t>(c->gen_part.n, (int64_t)grid * n_par));
+  c->gen_scratch.alloc(std::max<int64_t>(c->gen_scratch.n, (int64_t)grid * slots * kGenThreads));
+  CUDA_OK(cudaMemsetAsync(c->gen_part.p, 0, sizeof(float) * (size_t)(grid * n_par), c->stream));
+  GenArgs a{};
+  a.n_rows = n_rows;
+  a.in = in;
+  a.d_out = d_out;
+  a.d_in = d_in;
+  a.params = c->gen_par.p + par_off;
+  a.grad_partial = c->gen_part.p;
+  a.scratch = c->gen_scratch.p;
+  a.k = (int)c->K;
+  a.n_par = n_par;
+  auto k = gen_mlp_backward_kernel<IN, OUT, SKIP, LN, DIN>;
+  const size_t smem = gen_backward_smem(IN, OUT);
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, kGenThreads, smem, c->stream>>>(a);
+  check_launch(c);
+  reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->gen_part.p, grid, n_par,
+                                                                          c->mgrads.p + par_off);
+  check_launch(c);
+}
+
+void require_model(hgnn_ctx* c) {
+  require_ready(c);
+  if (!c->model_configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_configure has not been called");
+  if (!c->model_params_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_params_upload has not been called");
+  if (!c->model_data_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_set_data has not been called");
+}
+
+// compute_gradients (model.cpp:556-567) on the device; rank-averaged
+// gradients in mgrads, loss in c->last_loss.
+void model_compute_gradients(hgnn_ctx* c) {
+  const int64_t H = c->H, nl = c->nl;
+  ensure_buffers(c);
+  {  // encoders (model.cpp:289-294), every row / edge
+    Timed t(c, HGNN_K_ENCODE);
+    gen_forward<3, 64, true, true>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
+    gen_forward<7, 64, true, true>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
+  }
+  // message passing (model.cpp:295-300)
+  run_forward(c);
+  // decoder on local rows (model.cpp:303-306)
+  c->y.alloc(std::max<int64_t>(nl * c->fy, 1));
+  c->dy.alloc(std::max<int64_t>(nl * c->fy, 1));
+  {
+    Timed t(c, HGNN_K_DECODE);
+    gen_forward<64, 3, true, false>(c, nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
+  }
+  Timed t_loss(c, HGNN_K_LOSS_ADAM);
+  // consistent loss (model.cpp:455-480) and its adjoint (model.cpp:482-500)
+  c->loss_part.alloc(2 * kLossBlocks);
+  c->loss_st.alloc(3);
+  loss_partial_kernel<<<kLossBlocks, kLossThreads, 0, c->stream>>>(c->y.p, c->target.p, c->node_inv.p, nl,
+                                                                   (int)c->fy, c->loss_part.p);
+  check_launch(c);
+  loss_final_kernel<<<1, 32, 0, c->stream>>>(c->loss_part.p, kLossBlocks, c->loss_st.p);
+  check_launch(c);
+  if (c->nranks > 1) NCCL_OK(ncclAllReduce(c->loss_st.p, c->loss_st.p, 2, ncclDouble, ncclSum, c->comm, c->stream));
+  loss_seed_kernel<<<1, 32, 0, c->stream>>>(c->loss_st.p, (int)c->fy, c->nranks);
+  check_launch(c);
+  loss_backward_kernel<<<blocks_for(nl * c->fy), kEwThreads, 0, c->stream>>>(
+      c->y.p, c->target.p, c->node_inv.p, c->loss_st.p + 2, nl, (int)c->fy, c->dy.p);
+  check_launch(c);
+  t_loss.stop();
+  {  // decoder backward (model.cpp:402-409): adjoint of x_M on local rows, halo rows 0
+    Timed t(c, HGNN_K_DECODE);
+    CUDA_OK(cudaMemsetAsync(c->dx.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
+    gen_backward<64, 3, true, false, true>(c, nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
+  }
+  // message-passing backward (model.cpp:411-415), de_M = 0 (model.cpp:412)
+  CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * H), c->stream));
+  run_backward(c);
+  CUDA_OK(cudaMemcpyAsync(c->mgrads.p + c->off_mp, c->grads.p, sizeof(double) * (size_t)c->n_mp_par,
+                          cudaMemcpyDeviceToDevice, c->stream));
+  {  // encoder backward (model.cpp:417-423)
+    Timed t(c, HGNN_K_ENCODE);
+    gen_backward<3, 64, true, true, false>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
+    gen_backward<7, 64, true, true, false>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
+  }
+  // average over ranks (model.cpp:516-531)
+  if (c->nranks > 1) {
+    NCCL_OK(ncclAllReduce(c->mgrads.p, c->mgrads.p, (size_t)c->n_full, ncclDouble, ncclSum, c->comm, c->stream));
+    scale_f64_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mgrads.p, c->n_full,
+                                                                           1.0 / (double)c->nranks);
+    check_launch(c);
+  }
+  double st[2];
+  CUDA_OK(cudaMemcpyAsync(st, c->loss_st.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  c->last_loss = st[0] / (st[1] * (double)c->fy);
+}
+
+// fp32 / tf32 images of the parameters from the fp64 master copy.
+void model_refresh_params(hgnn_ctx* c) {
+  f64_to_f32_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->n_full, c->gen_par.p);
+  check_launch(c);
+  const double* mp = c->mparams.p + c->off_mp;
+  f64_to_f32_kernel<<<blocks_for(c->n_mp_par), kEwThreads, 0, c->stream>>>(mp, c->n_mp_par, c->par.p);
+  check_launch(c);
+  gather_f64_to_f32_kernel<<<blocks_for(c->n_mp_par), kEwThreads, 0, c->stream>>>(mp, c->pt_src.p, c->n_mp_par,
+                                                                                  c->par_t.p);
+  check_launch(c);
+  if (c->ch_map.n > 0) {
+    chunk_refresh_kernel<<<blocks_for(c->ch_map.n), kEwThreads, 0, c->stream>>>(mp, c->ch_map.p, c->ch_map.n,
+                                                                              c->chunks.p);
+    check_launch(c);
+  }
+  if (c->bch_map.n > 0) {
+    chunk_refresh_kernel<<<blocks_for(c->bch_map.n), kEwThreads, 0, c->stream>>>(mp, c->bch_map.p, c->bch_map.n,
+                                                                                c->bchunks.p);
+    check_launch(c);
+  }
+}
+
+// Device-refresh maps of the MP block (same element placement as the host
+// builders in hgnn_params_upload).
+void build_refresh_maps(hgnn_ctx* c) {
+  const int H = (int)c->H, K = (int)c->K;
+  std::vector<int32_t> pt((size_t)c->n_mp_par);
+  std::vector<uint32_t> ch, bch;
+  int64_t off = 0;
+  for (int64_t m = 0; m < c->M; ++m)
+    for (int which = 0; which < 2; ++which) {
+      const int in_dim = (which == 0 ? 3 : 2) * H;
+      for (int l = 0; l < K + 2; ++l) {
+        const int rin = l == 0 ? in_dim : H;
+        const int64_t wo = off + mlp_w_offset(l, in_dim, H), bo = off + mlp_b_offset(l, in_dim, H);
+        for (int i = 0; i < rin; ++i)
+          for (int j = 0; j < H; ++j) pt[(size_t)(wo + (int64_t)j * rin + i)] = (int32_t)(wo + (int64_t)i * H + j);
+        for (int j = 0; j < H; ++j) pt[(size_t)(bo + j)] = (int32_t)(bo + j);
+      }
+      if (tc_eligible(c)) {
+        const int64_t base = (int64_t)ch.size();
+        ch.resize((size_t)(base + chunk_floats_fwd(in_dim, H, K)));
+        chunk_layout_fwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
+          ch[(size_t)pos] = (uint32_t)(off + src) | (lo ? 0x80000000u : 0u);
+        });
+      }
+      if (H == 64) {
+        const int64_t base = (int64_t)bch.size();
+        bch.resize((size_t)(base + chunk_floats_bwd(in_dim, H, K)));
+        chunk_layout_bwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
+          bch[(size_t)pos] = (uint32_t)(off + src) | (lo ? 0x80000000u : 0u);
+        });
+      }
+      off += mlp_param_count(in_dim, H, K);
+    }
+  c->pt_src.upload(pt.data(), (int64_t)pt.size(), c->stream);
+  c->ch_map.upload(ch.data(), (int64_t)ch.size(), c->stream);
+  c->bch_map.upload(bch.data(), (int64_t)bch.size(), c->stream);
+}
+
+
+}  // namespace
+
+extern "C" {
+
+// ---- model level ----------------------------------------
+int hgnn_model_configure(hgnn_ctx* c, int64_t in_node_dim, int64_t in_edge_dim, int64_t out_dim) {
+  return guarded([&] {
+    bind(c);
+    if (!c->configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_configure has not been called");
+    if (c->H != kGenH) fail(HGNN_ERR_CONFIG, "model level: hidden width 64 only");
+    if (!gen_supported(in_node_dim, in_edge_dim, out_dim))
+      fail(HGNN_ERR_CONFIG, "model level: feature widths (F_x, F_e, F_y) = (3, 7, 3) supported");
+    c->fx = in_node_dim;
+    c->fe = in_edge_dim;
+    c->fy = out_dim;
+    const int K = (int)c->K;
+    c->n_ne = gen_param_count((int)c->fx, kGenH, K, true, true);
+    c->n_ee = gen_param_count((int)c->fe, kGenH, K, true, true);
+    c->n_dec = gen_param_count(kGenH, (int)c->fy, K, true, false);
+    c->off_ne = 0;
+    c->off_ee = c->n_ne;
+    c->off_mp = c->off_ee + c->n_ee;
+    c->off_dec = c->off_mp + c->n_mp_par;
+    c->n_full = c->off_dec + c->n_dec;
+    c->model_configured = true;
+    c->model_params_ready = c->model_data_ready = false;
+  });
+}
+
+int64_t hgnn_model_param_count(hgnn_ctx* c) { return c && c->model_configured ? c->n_full : -1; }
+
+int hgnn_model_params_upload(hgnn_ctx* c, const double* params, int64_t count) {
+  return guarded([&] {
+    bind(c);
+    if (!c->model_configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_configure has not been called");
+    if (count != c->n_full)
+      fail(HGNN_ERR_SHAPE, "hgnn_model_params_upload: expected " + std::to_string(c->n_full) + " values");
+    const int rc = hgnn_params_upload(c, params + c->off_mp, c->n_mp_par);
+    if (rc != HGNN_OK) fail(rc, hgnn_last_error());
+    c->mparams.upload(params, count, c->stream);
+    c->mgrads.alloc(count);
+    c->adam_m.alloc(count);
+    c->adam_v.alloc(count);
+    CUDA_OK(cudaMemsetAsync(c->adam_m.p, 0, sizeof(double) * (size_t)count, c->stream));
+    CUDA_OK(cudaMemsetAsync(c->adam_v.p, 0, sizeof(double) * (size_t)count, c->stream));
+    c->adam_step = 0;
+    c->gen_par.alloc(count);
+    f64_to_f32_kernel<<<blocks_for(count), kEwThreads, 0, c->stream>>>(c->mparams.p, count, c->gen_par.p);
+    check_launch(c);
+    build_refresh_maps(c);
+    c->nonfinite.alloc(1);
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->model_params_ready = true;
+  });
+}
+
+int hgnn_model_params_download(hgnn_ctx* c, double* params) {
+  return guarded([&] {
+    bind(c);
+    if (!c->model_params_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_params_upload has not been called");
+    CUDA_OK(cudaMemcpy(params, c->mparams.p, sizeof(double) * (size_t)c->n_full, cudaMemcpyDeviceToHost));
+  });
+}
+
+int hgnn_model_set_data(hgnn_ctx* c, const double* node_features, const double* edge_features,
+                        const double* target) {
+  return guarded([&] {
+    bind(c);
+    require_ready(c);
+    if (!c->model_configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_configure has not been called");
+    if (!node_features || !edge_features) fail(HGNN_ERR_SHAPE, "hgnn_model_set_data: null features");
+    if (!c->node_inv.p && c->nl > 0)
+      fail(HGNN_ERR_UNINITIALIZED, "hgnn_model_set_data: the graph was uploaded without node_inv_degree");
+    ensure_buffers(c);
+    c->node_feat.alloc(std::max<int64_t>(c->rows * c->fx, 1));
+    rows_to_device(c, node_features, c->rows * c->fx, c->node_feat.p);
+    c->edge_feat.alloc(std::max<int64_t>(c->ne * c->fe, 1));
+    edges_cols_to_device(c, edge_features, (int)c->fe, c->edge_feat.p);  // edge-id order -> slots
+    c->target.alloc(std::max<int64_t>(c->nl * c->fy, 1));
+    if (target) {
+      rows_to_device(c, target, c->nl * c->fy, c->target.p);
+    } else {  // autoencoding (model.cpp:605-607): target = local rows of the node features
+      if (c->fy != c->fx) fail(HGNN_ERR_SHAPE, "autoencoding target needs out_dim == in_node_dim");
+      CUDA_OK(cudaMemcpyAsync(c->target.p, c->node_feat.p, sizeof(float) * (size_t)(c->nl * c->fy),
+                              cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->model_data_ready = true;
+  });
+}
+
+int hgnn_compute_gradients(hgnn_ctx* c, double* loss, double* grads, double* y) {
+  return guarded([&] {
+    bind(c);
+    require_model(c);
+    model_compute_gradients(c);
+    if (loss) *loss = c->last_loss;
+    if (grads) CUDA_OK(cudaMemcpy(grads, c->mgrads.p, sizeof(double) * (size_t)c->n_full, cudaMemcpyDeviceToHost));
+    if (y) rows_to_host(c, c->y.p, c->nl * c->fy, y);
+  });
+}
+
+int hgnn_train_step(hgnn_ctx* c, double lr, double beta1, double beta2, double eps, double* loss) {
+  return guarded([&] {
+    bind(c);
+    require_model(c);
+    model_compute_gradients(c);
+    c->adam_step += 1;
+    const double bc1 = 1.0 - std::pow(beta1, (double)c->adam_step);
+    const double bc2 = 1.0 - std::pow(beta2, (double)c->adam_step);
+    Timed t(c, HGNN_K_LOSS_ADAM);
+    CUDA_OK(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), c->stream));
+    adam_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->mgrads.p, c->adam_m.p,
+                                                                     c->adam_v.p, c->n_full, lr, beta1, beta2, eps,
+                                                                     bc1, bc2, c->nonfinite.p);
+    check_launch(c);
+    int bad = 0;
+    CUDA_OK(cudaMemcpyAsync(&bad, c->nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    if (bad) fail(HGNN_ERR_OPTIMIZER, "adam_step: non-finite gradient");
+    model_refresh_params(c);
+    t.stop();
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    if (loss) *loss = c->last_loss;
+  });
+}
+
+}  // extern "C"
