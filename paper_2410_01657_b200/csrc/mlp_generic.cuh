@@ -88,9 +88,37 @@ __device__ __forceinline__ void gen_ln_stats(const float (&v)[N], float& mean, f
   inv_std = ptx::rsqrt_fast(((q[0] + q[1]) + (q[2] + q[3])) * (1.0f / N) + 1e-12f);
 }
 
-// acc[j] += sum_t v[t] W[t*NO + j] (W row-major, shared memory, warp-uniform reads)
+// acc[j] += sum_t v[t] W[t*NO + j] (W row-major, shared memory, warp-uniform
+// reads). Long inputs (NI >= 16) go through this thread's shared-memory
+// column (stride kGenThreads, conflict-free) so the t loop can stay rolled:
+// a fully unrolled 64 x 64 product is ~5K instructions and the kernels were
+// instruction-fetch bound.
 template <int NI, int NO>
-__device__ __forceinline__ void gen_gemv(float (&acc)[NO], const float (&v)[NI], const float* __restrict__ W) {
+__device__ __forceinline__ void gen_gemv(float (&acc)[NO], const float (&v)[NI], const float* __restrict__ W,
+                                         float* col) {
+  if (NI >= 16) {
+#pragma unroll
+    for (int t = 0; t < NI; ++t) col[t * kGenThreads] = v[t];
+#pragma unroll 2
+    for (int t = 0; t < NI; ++t) {
+      const float vt = col[t * kGenThreads];
+      if (NO % 4 == 0) {
+        const float4* w4 = reinterpret_cast<const float4*>(W + t * NO);
+#pragma unroll
+        for (int j = 0; j < NO / 4; ++j) {
+          const float4 w = w4[j];
+          acc[4 * j] = fmaf(vt, w.x, acc[4 * j]);
+          acc[4 * j + 1] = fmaf(vt, w.y, acc[4 * j + 1]);
+          acc[4 * j + 2] = fmaf(vt, w.z, acc[4 * j + 2]);
+          acc[4 * j + 3] = fmaf(vt, w.w, acc[4 * j + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NO; ++j) acc[j] = fmaf(vt, W[t * NO + j], acc[j]);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int t = 0; t < NI; ++t) {
     const float vt = v[t];
@@ -111,41 +139,33 @@ __device__ __forceinline__ void gen_gemv(float (&acc)[NO], const float (&v)[NI],
   }
 }
 
-// acc[t] += sum_j d[j] W[t*NO + j]  (adjoint product d W^T). Eight outputs
-// at a time so eight independent FMA chains are in flight.
+// acc[t] += sum_j d[j] W[t*NO + j]  (adjoint product d W^T): a rolled loop
+// over t writing this thread's shared-memory column, then one unrolled pass
+// adding the column into acc.
 template <int NI, int NO>
-__device__ __forceinline__ void gen_gemv_t(float (&acc)[NI], const float (&d)[NO], const float* __restrict__ W) {
-#pragma unroll
-  for (int t0 = 0; t0 < NI; t0 += 8) {
-    float s[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] = 0.f;
+__device__ __forceinline__ void gen_gemv_t(float (&acc)[NI], const float (&d)[NO], const float* __restrict__ W,
+                                           float* col) {
+#pragma unroll 2
+  for (int t = 0; t < NI; ++t) {
+    float p[4] = {0.f, 0.f, 0.f, 0.f};
     if (NO % 4 == 0) {
+      const float4* w4 = reinterpret_cast<const float4*>(W + t * NO);
 #pragma unroll
       for (int j = 0; j < NO / 4; ++j) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (t0 + u < NI) {
-            const float4 w = reinterpret_cast<const float4*>(W + (t0 + u) * NO)[j];
-            s[u] = fmaf(d[4 * j], w.x, s[u]);
-            s[u] = fmaf(d[4 * j + 1], w.y, s[u]);
-            s[u] = fmaf(d[4 * j + 2], w.z, s[u]);
-            s[u] = fmaf(d[4 * j + 3], w.w, s[u]);
-          }
-        }
+        const float4 w = w4[j];
+        p[0] = fmaf(d[4 * j], w.x, p[0]);
+        p[1] = fmaf(d[4 * j + 1], w.y, p[1]);
+        p[2] = fmaf(d[4 * j + 2], w.z, p[2]);
+        p[3] = fmaf(d[4 * j + 3], w.w, p[3]);
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < NO; ++j) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (t0 + u < NI) s[u] = fmaf(d[j], W[(t0 + u) * NO + j], s[u]);
-      }
+      for (int j = 0; j < NO; ++j) p[j % 4] = fmaf(d[j], W[t * NO + j], p[j % 4]);
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (t0 + u < NI) acc[t0 + u] += s[u];
+    col[t * kGenThreads] = (p[0] + p[1]) + (p[2] + p[3]);
   }
+#pragma unroll
+  for (int t = 0; t < NI; ++t) acc[t] += col[t * kGenThreads];
 }
 
 template <int N>
@@ -164,6 +184,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a)
   constexpr int H = kGenH;
   extern __shared__ __align__(16) float gsm[];
   const GenLayout L{IN, OUT, a.k};
+  float* col = gsm + ((a.n_par + 3) / 4) * 4 + threadIdx.x;  // this thread's column (kGenH x kGenThreads)
   gen_stage_params(gsm, a.params, a.n_par);
   __syncthreads();
   for (int64_t row = (int64_t)blockIdx.x * kGenThreads + threadIdx.x; row - threadIdx.x < a.n_rows;
@@ -175,13 +196,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a)
       gen_load_row<IN>(x, a.in + row * IN, valid);
 #pragma unroll
       for (int j = 0; j < H; ++j) h[j] = gsm[L.b(0) + j];
-      gen_gemv<IN, H>(h, x, gsm + L.w(0));
+      gen_gemv<IN, H>(h, x, gsm + L.w(0), col);
     }
     for (int l = 1; l <= a.k; ++l) {
       float u[H];
 #pragma unroll
       for (int j = 0; j < H; ++j) u[j] = gsm[L.b(l) + j];
-      gen_gemv<H, H>(u, h, gsm + L.w(l));
+      gen_gemv<H, H>(u, h, gsm + L.w(l), col);
       float mean, inv_std;
       gen_ln_stats<H>(u, mean, inv_std);
 #pragma unroll
@@ -190,11 +211,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a)
     float y[OUT];
 #pragma unroll
     for (int j = 0; j < OUT; ++j) y[j] = gsm[L.b(a.k + 1) + j];
-    gen_gemv<H, OUT>(y, h, gsm + L.w(a.k + 1));
+    gen_gemv<H, OUT>(y, h, gsm + L.w(a.k + 1), col);
     if (SKIP) {
       float x[IN];
       gen_load_row<IN>(x, a.in + row * IN, valid);
-      gen_gemv<IN, OUT>(y, x, gsm + L.skip());
+      gen_gemv<IN, OUT>(y, x, gsm + L.skip(), col);
     }
     if (OUT_LN) {
       float mean, inv_std;
@@ -308,6 +329,10 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
   float* sG = sSkip + SK_N;
   float* sA = sG + LN_N;
   float* sD = sA + kGenThreads * kGenRow;
+  // this thread's gemv column (kGenH x kGenThreads floats) aliases the A
+  // staging buffer: every use is separated from the dW tiles by the CTA
+  // barriers of load_linear / the staging
+  float* col = sA + threadIdx.x;
   if (SKIP)
     for (int i = threadIdx.x; i < IN * OUT; i += kGenThreads) sSkip[i] = __ldg(a.params + L.skip() + i);
   if (OUT_LN)
@@ -339,7 +364,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
         const float* W = load_linear(0);
 #pragma unroll
         for (int j = 0; j < H; ++j) h[j] = W[IN * H + j];
-        gen_gemv<IN, H>(h, x, W);
+        gen_gemv<IN, H>(h, x, W, col);
       }
 #pragma unroll
       for (int j = 0; j < H; ++j) S(s_h + j) = h[j];
@@ -348,7 +373,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
         const float* W = load_linear(l);
 #pragma unroll
         for (int j = 0; j < H; ++j) u[j] = W[H * H + j];
-        gen_gemv<H, H>(u, h, W);
+        gen_gemv<H, H>(u, h, W, col);
         float mean, inv_std;
         gen_ln_stats<H>(u, mean, inv_std);
 #pragma unroll
@@ -364,11 +389,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       const float* W = load_linear(K + 1);
 #pragma unroll
       for (int j = 0; j < OUT; ++j) y[j] = W[H * OUT + j];
-      gen_gemv<H, OUT>(y, h, W);
+      gen_gemv<H, OUT>(y, h, W, col);
       if (SKIP) {
         float x[IN];
         gen_load_row<IN>(x, a.in + row * IN, valid);
-        gen_gemv<IN, OUT>(y, x, sSkip);
+        gen_gemv<IN, OUT>(y, x, sSkip, col);
       }
       if (OUT_LN) {
         float mean, inv_std;
@@ -432,7 +457,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       }
 #pragma unroll
       for (int j = 0; j < H; ++j) dh[j] = 0.f;
-      gen_gemv_t<H, OUT>(dh, dy, load_linear(K + 1));
+      gen_gemv_t<H, OUT>(dh, dy, load_linear(K + 1), col);
     }
 
     // ---- hidden blocks in reverse (nn.cpp:259-274)
@@ -462,7 +487,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
       }
       gen_dw_tile<H, H>(gp + L.w(l), sA, sD);
       gen_db_tile<H>(gp + L.b(l), sD);
-      gen_gemv_t<H, H>(dh, du, load_linear(l));  // d_prev = d_u W^T + d_h
+      gen_gemv_t<H, H>(dh, du, load_linear(l), col);  // d_prev = d_u W^T + d_h
     }
     // ---- input projection (nn.cpp:277-281)
     if (DIN) {  // d_in = d_h W0^T (+ d_y W_skip^T), 16 input columns at a time

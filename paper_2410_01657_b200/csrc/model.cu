@@ -25,7 +25,7 @@ void gen_forward(hgnn_ctx* c, int64_t n_rows, const float* in, float* out, int64
   a.k = (int)c->K;
   a.n_par = n_par;
   auto k = gen_mlp_forward_kernel<IN, OUT, SKIP, LN>;
-  const size_t smem = (size_t)n_par * 4;
+  const size_t smem = (size_t)((n_par + 3) / 4) * 16 + (size_t)kGenH * kGenThreads * 4;  // params + gemv columns
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));
