@@ -30,6 +30,7 @@ enum {
   HGNN_ERR_UNINITIALIZED = 6,  /* UninitializedError */
   HGNN_ERR_SIZE = 7,           /* SizeError */
   HGNN_ERR_OPTIMIZER = 8,      /* OptimizerError */
+  HGNN_ERR_IO = 9,             /* IoError */
   HGNN_ERR_CUDA = 20,          /* device fault / missing GPU */
   HGNN_ERR_NCCL = 21,          /* NCCL failure */
   HGNN_ERR_INTERNAL = 22
@@ -89,6 +90,14 @@ int hgnn_graph_build(int64_t elements_per_axis, int64_t poly_order, int64_t num_
 void hgnn_graph_free(hgnn_host_graph* g);
 /* Zero-copy view of the built arrays (valid until hgnn_graph_free). */
 int hgnn_graph_view(const hgnn_host_graph* g, hgnn_graph_desc* out);
+/* Per-rank HGNNGRB1 graph files, byte-compatible with the reference's
+ * save_graph_binary / load_graph (io.cpp:200-309; replaces both for the binary
+ * format). The loader recomputes the reciprocal degrees and the CSR exactly
+ * as finalize_loaded_graph (io.cpp:152-161) and range-checks every index the
+ * device path dereferences; a loaded graph has num_ranks = 0 (not stored).
+ * Errors: HGNN_ERR_IO (missing/truncated/corrupt file, JSON dumps). */
+int hgnn_graph_save_binary(const hgnn_graph_desc* g, const char* path);
+int hgnn_graph_load_binary(const char* path, hgnn_host_graph** out);
 /* balanced_factors (mesh.cpp:154-176) */
 int hgnn_balanced_factors(int64_t num_ranks, int64_t elements_per_axis, int64_t out[3]);
 

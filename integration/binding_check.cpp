@@ -96,6 +96,7 @@ int main() {
   expect_throw<CollectiveError>(HGNN_ERR_COLLECTIVE, "collective");
   expect_throw<UninitializedError>(HGNN_ERR_UNINITIALIZED, "uninitialized");
   expect_throw<OptimizerError>(HGNN_ERR_OPTIMIZER, "optimizer");
+  expect_throw<IoError>(HGNN_ERR_IO, "io");
   expect_throw<Error>(HGNN_ERR_CUDA, "cuda");
   try {  // a bad partition request reaches the caller as PartitionError
     hgnn_host_graph* g = nullptr;

@@ -40,6 +40,7 @@ inline void check(int status, const char* where) {
     case HGNN_ERR_UNINITIALIZED: throw UninitializedError(msg);
     case HGNN_ERR_SIZE: throw SizeError(msg);
     case HGNN_ERR_OPTIMIZER: throw OptimizerError(msg);
+    case HGNN_ERR_IO: throw IoError(msg);
     default: throw Error(msg);  // device / NCCL / internal failures
   }
 }

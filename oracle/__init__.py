@@ -162,6 +162,11 @@ def ref_available() -> bool:
     return REF_LIB.exists()
 
 
+def ref_has_io() -> bool:
+    """True when oracle/_ref was built with the reference's io.cpp."""
+    return ref_available() and bool(ref_lib().ref_has_io())
+
+
 def ref_lib() -> C.CDLL:
     global _rlib
     if _rlib is None:
@@ -171,6 +176,8 @@ def ref_lib() -> C.CDLL:
         lib.ref_graph_build.restype = vp
         lib.ref_graph_build.argtypes = [C.c_int64] * 3 + [C.c_int] + [C.c_int64] * 3 + [C.c_int]
         lib.ref_graph_free.argtypes = [vp]
+        lib.ref_graph_save_binary.argtypes = [vp, C.c_int, C.c_char_p]
+        lib.ref_has_io.restype = C.c_int
         lib.ref_graph_sizes.argtypes = [vp, C.c_int, C.POINTER(C.c_int64)]
         i64p = C.POINTER(C.c_int64)
         lib.ref_graph_export.argtypes = [vp, C.c_int, i64p, f64p, f64p, f64p, i32p, i32p, i32p, i32p, f64p, f64p,
@@ -255,6 +262,14 @@ class RefGraph:
             "neighbors", "send_offsets", "send_rows", "recv_offsets", "recv_rows", "halo_to_local", "sync_local",
             "sync_offsets", "sync_slots")])
         return g
+
+    def save_binary(self, rank, path):
+        """The reference's own save_graph_binary (io.cpp:200-231) for one rank."""
+        rc = ref_lib().ref_graph_save_binary(self.h, rank, str(path).encode())
+        if rc == -2:
+            raise RuntimeError("io.cpp is not compiled into oracle/_ref (nlohmann/json.hpp not found)")
+        if rc != 0:
+            raise RuntimeError(ref_lib().ref_last_error().decode())
 
     def __del__(self):
         if getattr(self, "h", None):

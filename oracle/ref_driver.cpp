@@ -18,15 +18,20 @@
 #include <memory>
 #include <vector>
 
-// io.cpp is not built (it needs nlohmann/json, an external library); the
-// harness only references write_csv from the CSV writers, which the oracle
-// never calls.
+// io.cpp needs nlohmann/json (an external library). oracle/Makefile compiles
+// it in place when a copy of json.hpp is found in the image (-DHGNN_REF_IO);
+// otherwise the harness's one reference to it, write_csv, is stubbed (the
+// oracle never calls the CSV writers).
+#ifdef HGNN_REF_IO
+#include "hgnn/io.hpp"
+#else
 namespace hgnn {
 void write_csv(const std::string&, const std::vector<std::string>&,
                const std::vector<std::vector<std::string>>&) {
   throw IoError("write_csv is not available in the oracle build");
 }
 }  // namespace hgnn
+#endif
 
 using namespace hgnn;
 
@@ -209,6 +214,28 @@ void* ref_graph_build(int64_t E, int64_t p, int64_t R, int strategy, int64_t fx,
 }
 
 void ref_graph_free(void* h) { delete static_cast<RefGraph*>(h); }
+
+// save_graph_binary (io.cpp:200-231) of one rank; 0 = ok, -1 = error,
+// -2 = io.cpp not compiled into this oracle build.
+int ref_graph_save_binary(void* hnd, int rank, const char* path) {
+#ifdef HGNN_REF_IO
+  const auto& rg = *static_cast<RefGraph*>(hnd);
+  return guarded([&] {
+    save_graph_binary(path, rg.dg.graphs.at(static_cast<size_t>(rank)), rg.dg.halos.at(static_cast<size_t>(rank)));
+  });
+#else
+  (void)hnd, (void)rank, (void)path;
+  return -2;
+#endif
+}
+
+int ref_has_io() {
+#ifdef HGNN_REF_IO
+  return 1;
+#else
+  return 0;
+#endif
+}
 
 // out[0..8] = num_local, num_halo, num_edges, n_nbr, n_send_total, n_sync, n_sync_slots,
 //             max_buffer_rows, num_ranks

@@ -49,12 +49,16 @@ class OptimizerError(Error):
     """hgnn::OptimizerError (error.hpp:51-55)."""
 
 
+class IoError(Error):
+    """hgnn::IoError (error.hpp:69-73)."""
+
+
 class DeviceError(Error):
     """CUDA / NCCL failure or missing B200."""
 
 
 _CODES = {1: ShapeError, 2: ConfigError, 3: PartitionError, 4: CollectiveError, 5: IntegrityError,
-          6: UninitializedError, 7: SizeError, 8: OptimizerError, 20: DeviceError, 21: DeviceError, 22: Error}
+          6: UninitializedError, 7: SizeError, 8: OptimizerError, 9: IoError, 20: DeviceError, 21: DeviceError, 22: Error}
 
 MODE_NONE, MODE_A2A, MODE_NA2A = 0, 1, 2
 MODES = {"none": MODE_NONE, "a2a": MODE_A2A, "na2a": MODE_NA2A}
@@ -113,6 +117,8 @@ def _load() -> C.CDLL:
         "hgnn_graph_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, i64p, C.c_int32, C.POINTER(vp)]),
         "hgnn_graph_free": (None, [vp]),
         "hgnn_graph_view": (C.c_int, [vp, C.POINTER(GraphDesc)]),
+        "hgnn_graph_save_binary": (C.c_int, [C.POINTER(GraphDesc), C.c_char_p]),
+        "hgnn_graph_load_binary": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
         "hgnn_balanced_factors": (C.c_int, [C.c_int64, C.c_int64, i64p]),
         "hgnn_param_count": (C.c_int64, [C.c_int64] * 6),
         "hgnn_init_params": (C.c_int, [C.c_int64] * 6 + [C.c_uint64, f64p]),
@@ -157,7 +163,8 @@ def _load() -> C.CDLL:
 
 
 LIB = _load()
-EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_graph_view", "hgnn_balanced_factors",
+EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_graph_view", "hgnn_graph_save_binary",
+            "hgnn_graph_load_binary", "hgnn_balanced_factors",
             "hgnn_param_count", "hgnn_init_params", "hgnn_mp_param_range", "hgnn_device_count", "hgnn_nccl_unique_id",
             "hgnn_ctx_create", "hgnn_ctx_destroy", "hgnn_ctx_stream", "hgnn_graph_upload", "hgnn_configure",
             "hgnn_params_upload", "hgnn_mp_forward", "hgnn_mp_backward", "hgnn_get_trace",

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -167,6 +168,21 @@ void finalize_view(HostGraph& hg) {
   v.sync_local = hg.sync_local.data();
   v.sync_offsets = hg.sync_off.data();
   v.sync_slots = hg.sync_slots.data();
+}
+
+// In/out CSR by counting sort, ascending edge id per node (graph.cpp:122-136).
+void build_csr(HostGraph& hg, int64_t rows) {
+  const int64_t ne = static_cast<int64_t>(hg.edge_src.size());
+  auto csr = [&](const std::vector<int32_t>& key, std::vector<int32_t>& off, std::vector<int32_t>& ids) {
+    off.assign(static_cast<size_t>(rows + 1), 0);
+    for (int64_t e = 0; e < ne; ++e) off[static_cast<size_t>(key[static_cast<size_t>(e)]) + 1]++;
+    for (int64_t i = 0; i < rows; ++i) off[static_cast<size_t>(i + 1)] += off[static_cast<size_t>(i)];
+    ids.resize(static_cast<size_t>(ne));
+    std::vector<int32_t> cur(off.begin(), off.end() - 1);
+    for (int64_t e = 0; e < ne; ++e) ids[static_cast<size_t>(cur[static_cast<size_t>(key[static_cast<size_t>(e)])]++)] = static_cast<int32_t>(e);
+  };
+  csr(hg.edge_dst, hg.in_off, hg.in_edges);
+  csr(hg.edge_src, hg.out_off, hg.out_edges);
 }
 
 std::unique_ptr<HostGraph> build(int64_t E, int64_t p, int64_t R, int strategy, const int64_t* factors,
@@ -402,16 +418,7 @@ std::unique_ptr<HostGraph> build(int64_t E, int64_t p, int64_t R, int strategy, 
   }
 
   // ---- CSR by counting sort (graph.cpp:122-136).
-  auto csr = [&](const std::vector<int32_t>& key, std::vector<int32_t>& off, std::vector<int32_t>& ids) {
-    off.assign(static_cast<size_t>(rows + 1), 0);
-    for (int64_t e = 0; e < ne; ++e) off[static_cast<size_t>(key[static_cast<size_t>(e)]) + 1]++;
-    for (int64_t i = 0; i < rows; ++i) off[static_cast<size_t>(i + 1)] += off[static_cast<size_t>(i)];
-    ids.resize(static_cast<size_t>(ne));
-    std::vector<int32_t> cur(off.begin(), off.end() - 1);
-    for (int64_t e = 0; e < ne; ++e) ids[static_cast<size_t>(cur[static_cast<size_t>(key[static_cast<size_t>(e)])]++)] = static_cast<int32_t>(e);
-  };
-  csr(hg->edge_dst, hg->in_off, hg->in_edges);
-  csr(hg->edge_src, hg->out_off, hg->out_edges);
+  build_csr(*hg, rows);
 
   // ---- global max send-mask length (graph.cpp:616-621): the largest
   //      lattice-box intersection between two distinct ranks.
@@ -429,6 +436,184 @@ std::unique_ptr<HostGraph> build(int64_t E, int64_t p, int64_t R, int strategy, 
       max_rows = std::max(max_rows, cnt);
     }
 
+  hg->view.num_local = nl;
+  hg->view.num_halo = nh;
+  hg->view.num_edges = ne;
+  hg->view.max_buffer_rows = max_rows;
+  finalize_view(*hg);
+  return hg;
+}
+
+// ---- HGNNGRB1 per-rank graph files (io.cpp:200-309). Little-endian:
+//   "HGNNGRB1", i64 rank, num_local, num_halo, num_edges, F_x = 3, F_e = 7,
+//   vec<i64> global_ids, vec<f64> positions (rows*3), vec<i32> edge_src,
+//   edge_dst, node_degree, edge_degree, i64 n_nbr, n_nbr x {i32 neighbor,
+//   vec<i32> send_mask, vec<i32> recv_mask}, vec<i32> halo_to_local,
+//   i64 max_buffer_rows, i64 n_groups, n_groups x {i32 local, vec<i32> slots};
+// vec<T> = i64 length + raw elements (io.cpp:47-74).
+constexpr char kGraphMagic[8] = {'H', 'G', 'N', 'N', 'G', 'R', 'B', '1'};
+
+struct FileWriter {
+  std::FILE* f;
+  std::string path;
+  void raw(const void* p, size_t n) {
+    if (n && std::fwrite(p, 1, n, f) != n) fail(HGNN_ERR_IO, "cannot write " + path);
+  }
+  template <class T>
+  void pod(T v) { raw(&v, sizeof(T)); }
+  template <class T>
+  void vec(const T* p, int64_t n) {
+    pod<int64_t>(n);
+    raw(p, sizeof(T) * static_cast<size_t>(n));
+  }
+};
+
+struct FileReader {
+  std::FILE* f;
+  std::string path;
+  int64_t left;  // bytes not yet consumed
+  void raw(void* p, size_t n) {
+    if (static_cast<int64_t>(n) > left || (n && std::fread(p, 1, n, f) != n))
+      fail(HGNN_ERR_IO, path + ": truncated graph file");
+    left -= static_cast<int64_t>(n);
+  }
+  template <class T>
+  T pod() {
+    T v{};
+    raw(&v, sizeof(T));
+    return v;
+  }
+  template <class T>
+  std::vector<T> vec() {
+    const int64_t n = pod<int64_t>();
+    if (n < 0 || n > left / static_cast<int64_t>(sizeof(T))) fail(HGNN_ERR_IO, path + ": bad vector length");
+    std::vector<T> v(static_cast<size_t>(n));
+    raw(v.data(), sizeof(T) * v.size());
+    return v;
+  }
+};
+
+struct File {
+  std::FILE* f;
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+void save_binary(const hgnn_graph_desc& g, const std::string& path) {
+  File file{std::fopen(path.c_str(), "wb")};
+  if (!file.f) fail(HGNN_ERR_IO, "cannot write " + path);
+  FileWriter w{file.f, path};
+  const int64_t rows = g.num_local + g.num_halo, ne = g.num_edges;
+  w.raw(kGraphMagic, 8);
+  w.pod<int64_t>(g.rank);
+  w.pod<int64_t>(g.num_local);
+  w.pod<int64_t>(g.num_halo);
+  w.pod<int64_t>(ne);
+  w.pod<int64_t>(3);  // F_x
+  w.pod<int64_t>(7);  // F_e
+  w.vec(g.global_ids, rows);
+  w.vec(g.positions, rows * 3);
+  w.vec(g.edge_src, ne);
+  w.vec(g.edge_dst, ne);
+  w.vec(g.node_degree, g.num_local);
+  w.vec(g.edge_degree, ne);
+  w.pod<int64_t>(g.num_neighbors);
+  for (int32_t n = 0; n < g.num_neighbors; ++n) {
+    w.pod<int32_t>(g.neighbors[n]);
+    w.vec(g.send_rows + g.send_offsets[n], g.send_offsets[n + 1] - g.send_offsets[n]);
+    w.vec(g.recv_rows + g.recv_offsets[n], g.recv_offsets[n + 1] - g.recv_offsets[n]);
+  }
+  w.vec(g.halo_to_local, g.num_halo);
+  w.pod<int64_t>(g.max_buffer_rows);
+  w.pod<int64_t>(g.num_sync_groups);
+  for (int64_t t = 0; t < g.num_sync_groups; ++t) {
+    w.pod<int32_t>(g.sync_local[t]);
+    w.vec(g.sync_slots + g.sync_offsets[t], g.sync_offsets[t + 1] - g.sync_offsets[t]);
+  }
+  if (std::fflush(file.f) != 0) fail(HGNN_ERR_IO, "cannot write " + path);
+}
+
+void check_index(const std::vector<int32_t>& v, int64_t lo, int64_t hi, const std::string& what) {
+  for (int32_t x : v)
+    if (x < lo || x >= hi) fail(HGNN_ERR_IO, what + " index out of range");
+}
+
+std::unique_ptr<HostGraph> load_binary(const std::string& path) {
+  File file{std::fopen(path.c_str(), "rb")};
+  if (!file.f) fail(HGNN_ERR_IO, "cannot open " + path);
+  std::fseek(file.f, 0, SEEK_END);
+  const int64_t size = std::ftell(file.f);
+  std::fseek(file.f, 0, SEEK_SET);
+  FileReader in{file.f, path, size};
+  char magic[8] = {};
+  if (size < 8) fail(HGNN_ERR_IO, path + ": not an HGNNGRB1 graph file");
+  in.raw(magic, 8);
+  if (std::memcmp(magic, kGraphMagic, 8) != 0)
+    fail(HGNN_ERR_IO, path + ": not an HGNNGRB1 graph file (JSON graph dumps are not supported)");
+  auto hg = std::make_unique<HostGraph>();
+  const int64_t rank = in.pod<int64_t>(), nl = in.pod<int64_t>(), nh = in.pod<int64_t>(), ne = in.pod<int64_t>();
+  in.pod<int64_t>();  // F_x
+  in.pod<int64_t>();  // F_e
+  if (rank < 0 || nl < 0 || nh < 0 || ne < 0 || nl + nh >= (int64_t{1} << 31) || ne >= (int64_t{1} << 31))
+    fail(HGNN_ERR_IO, path + ": bad header");
+  const int64_t rows = nl + nh;
+  hg->global_ids = in.vec<int64_t>();
+  hg->positions = in.vec<double>();
+  if (static_cast<int64_t>(hg->positions.size()) != rows * 3) fail(HGNN_ERR_IO, path + ": bad positions");
+  hg->edge_src = in.vec<int32_t>();
+  hg->edge_dst = in.vec<int32_t>();
+  if (static_cast<int64_t>(hg->edge_src.size()) != ne || static_cast<int64_t>(hg->edge_dst.size()) != ne)
+    fail(HGNN_ERR_IO, path + ": bad adjacency");
+  hg->node_degree = in.vec<int32_t>();
+  hg->edge_degree = in.vec<int32_t>();
+  const int64_t n_nbr = in.pod<int64_t>();
+  if (n_nbr < 0 || n_nbr > in.left / 20) fail(HGNN_ERR_IO, path + ": bad neighbour count");
+  hg->send_off.push_back(0);
+  hg->recv_off.push_back(0);
+  for (int64_t n = 0; n < n_nbr; ++n) {
+    hg->nbr.push_back(in.pod<int32_t>());
+    const auto sm = in.vec<int32_t>(), rm = in.vec<int32_t>();
+    hg->send_rows.insert(hg->send_rows.end(), sm.begin(), sm.end());
+    hg->recv_rows.insert(hg->recv_rows.end(), rm.begin(), rm.end());
+    hg->send_off.push_back(static_cast<int32_t>(hg->send_rows.size()));
+    hg->recv_off.push_back(static_cast<int32_t>(hg->recv_rows.size()));
+  }
+  hg->halo_to_local = in.vec<int32_t>();
+  const int64_t max_rows = in.pod<int64_t>();
+  const int64_t n_groups = in.pod<int64_t>();
+  if (n_groups < 0 || n_groups > in.left / 12) fail(HGNN_ERR_IO, path + ": bad sync-group count");
+  hg->sync_off.push_back(0);
+  for (int64_t t = 0; t < n_groups; ++t) {
+    hg->sync_local.push_back(in.pod<int32_t>());
+    const auto sl = in.vec<int32_t>();
+    hg->sync_slots.insert(hg->sync_slots.end(), sl.begin(), sl.end());
+    hg->sync_off.push_back(static_cast<int32_t>(hg->sync_slots.size()));
+  }
+  // The reference's checks (io.cpp:300-305), then the ones the device path
+  // relies on: every index the kernels dereference is in range.
+  if (static_cast<int64_t>(hg->global_ids.size()) != rows) fail(HGNN_ERR_IO, path + ": global_ids length mismatch");
+  if (static_cast<int64_t>(hg->node_degree.size()) != nl) fail(HGNN_ERR_IO, path + ": node_degree length mismatch");
+  if (static_cast<int64_t>(hg->edge_degree.size()) != ne) fail(HGNN_ERR_IO, path + ": edge_degree length mismatch");
+  if (static_cast<int64_t>(hg->halo_to_local.size()) != nh) fail(HGNN_ERR_IO, path + ": halo_to_local length mismatch");
+  check_index(hg->edge_src, 0, rows, path + ": edge_src");
+  check_index(hg->edge_dst, 0, rows, path + ": edge_dst");
+  check_index(hg->send_rows, 0, nl, path + ": send mask");
+  check_index(hg->recv_rows, nl, rows, path + ": recv mask");
+  check_index(hg->sync_local, 0, nl, path + ": sync group");
+  check_index(hg->sync_slots, -1, rows, path + ": sync slot");
+  for (int32_t d : hg->node_degree)
+    if (d < 1) fail(HGNN_ERR_IO, path + ": node_degree must be >= 1");
+  for (int32_t d : hg->edge_degree)
+    if (d < 1) fail(HGNN_ERR_IO, path + ": edge_degree must be >= 1");
+  // finalize_loaded_graph (io.cpp:152-161): reciprocal degrees + CSR.
+  hg->node_inv.resize(hg->node_degree.size());
+  for (size_t i = 0; i < hg->node_degree.size(); ++i) hg->node_inv[i] = 1.0 / static_cast<double>(hg->node_degree[i]);
+  hg->edge_inv.resize(hg->edge_degree.size());
+  for (size_t i = 0; i < hg->edge_degree.size(); ++i) hg->edge_inv[i] = 1.0 / static_cast<double>(hg->edge_degree[i]);
+  build_csr(*hg, rows);
+  hg->view.rank = static_cast<int32_t>(rank);
+  hg->view.num_ranks = 0;  // not stored in the file; the context carries the rank count
   hg->view.num_local = nl;
   hg->view.num_halo = nh;
   hg->view.num_edges = ne;
@@ -466,6 +651,22 @@ int hgnn_graph_view(const hgnn_host_graph* g, hgnn_graph_desc* out) {
   return guarded([&] {
     if (!g || !out) fail(HGNN_ERR_CONFIG, "hgnn_graph_view: null argument");
     *out = g->g->view;
+  });
+}
+
+int hgnn_graph_save_binary(const hgnn_graph_desc* g, const char* path) {
+  return guarded([&] {
+    if (!g || !path) fail(HGNN_ERR_CONFIG, "hgnn_graph_save_binary: null argument");
+    save_binary(*g, path);
+  });
+}
+
+int hgnn_graph_load_binary(const char* path, hgnn_host_graph** out) {
+  return guarded([&] {
+    if (!path || !out) fail(HGNN_ERR_CONFIG, "hgnn_graph_load_binary: null argument");
+    auto h = std::make_unique<hgnn_host_graph>();
+    h->g = load_binary(path);
+    *out = h.release();
   });
 }
 

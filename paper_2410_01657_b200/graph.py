@@ -89,6 +89,24 @@ def build_rank_graph(elements_per_axis: int, poly_order: int, num_ranks: int, ra
         fac = (C.c_int64 * 3)(*factors)
     N.check(N.LIB.hgnn_graph_build(elements_per_axis, poly_order, num_ranks, STRATEGIES[strategy],
                                    C.cast(fac, N.i64p) if fac is not None else None, rank, C.byref(h)))
+    return _take(h)
+
+
+def load_graph_binary(path) -> RankGraph:
+    """load_graph for HGNNGRB1 files (io.cpp:241-309); num_ranks is 0 (not stored)."""
+    h = C.c_void_p()
+    N.check(N.LIB.hgnn_graph_load_binary(str(path).encode(), C.byref(h)))
+    return _take(h)
+
+
+def save_graph_binary(graph: RankGraph, path) -> None:
+    """save_graph_binary (io.cpp:200-231), byte-identical to the reference's."""
+    d = graph.desc()
+    N.check(N.LIB.hgnn_graph_save_binary(C.byref(d), str(path).encode()))
+
+
+def _take(h) -> RankGraph:
+    """Copy a native hgnn_host_graph into numpy arrays and free it."""
     try:
         d = N.GraphDesc()
         N.check(N.LIB.hgnn_graph_view(h, C.byref(d)))
@@ -110,7 +128,8 @@ def build_rank_graph(elements_per_axis: int, poly_order: int, num_ranks: int, ra
             out_offsets=_arr(d.out_offsets, rows + 1, np.int32), out_edges=_arr(d.out_edges, ne, np.int32),
             neighbors=_arr(d.neighbors, nn, np.int32),
             send_offsets=_arr(d.send_offsets, nn + 1, np.int32), send_rows=_arr(d.send_rows, ns, np.int32),
-            recv_offsets=_arr(d.recv_offsets, nn + 1, np.int32), recv_rows=_arr(d.recv_rows, nh, np.int32),
+            recv_offsets=_arr(d.recv_offsets, nn + 1, np.int32),
+            recv_rows=_arr(d.recv_rows, d.recv_offsets[nn] if nn else 0, np.int32),
             halo_to_local=_arr(d.halo_to_local, nh, np.int32),
             sync_local=_arr(d.sync_local, nsync, np.int32), sync_offsets=_arr(d.sync_offsets, nsync + 1, np.int32),
             sync_slots=_arr(d.sync_slots, nslots, np.int32),

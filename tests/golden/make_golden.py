@@ -44,6 +44,18 @@ def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
+def binary_shas(ref, R) -> list[str]:
+    """sha256 of the reference's own save_graph_binary file (io.cpp:200-231) per rank."""
+    import tempfile
+    out = []
+    with tempfile.TemporaryDirectory() as d:
+        for r in range(R):
+            f = Path(d) / f"r{r}.bin"
+            ref.save_binary(r, f)
+            out.append(hashlib.sha256(f.read_bytes()).hexdigest())
+    return out
+
+
 def mp_inputs(graph_ranks, H, seed):
     rng = np.random.default_rng(seed)
     x0 = [rng.uniform(-1, 1, (g.num_local + g.num_halo, H)) for g in graph_ranks]
@@ -63,7 +75,8 @@ def main() -> None:
         graphs[key] = {"E": E, "p": p, "R": R, "strategy": strat, "factors": fac,
                        "ranks": [{**{f: sha(getattr(g, f)) for f in GRAPH_FIELDS},
                                   "num_local": g.num_local, "num_halo": g.num_halo, "num_edges": g.num_edges,
-                                  "max_buffer_rows": g.max_buffer_rows} for g in ref.ranks]}
+                                  "max_buffer_rows": g.max_buffer_rows,
+                                  "binary_sha256": b} for g, b in zip(ref.ranks, binary_shas(ref, R))]}
     params = {}
     for H, M, k in [(8, 4, 2), (32, 4, 5), (64, 4, 5)]:
         for seed in (0, 3):
