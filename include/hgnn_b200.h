@@ -51,7 +51,7 @@ const char* hgnn_last_error(void);
 /* (graph.hpp:16-65), flattened. Lists over neighbours / sync groups are CSR. */
 /* ========================================================================== */
 typedef struct {
-  int32_t rank, num_ranks;
+  int32_t rank, num_ranks; /* num_ranks 0 = unknown (the context's count is used) */
   int64_t num_local, num_halo, num_edges;
   const int64_t* global_ids;        /* [rows]        graph.hpp:22 */
   const double* positions;          /* [rows*3]      (nullable for upload) */

@@ -672,7 +672,9 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
   return guarded([&] {
     bind(c);
     if (!g) fail(HGNN_ERR_CONFIG, "hgnn_graph_upload: null graph");
-    if (g->rank != c->rank || g->num_ranks != c->nranks)
+    // num_ranks == 0: not known to the caller (a loaded HGNNGRB1 file, or the
+    // reference-side GraphDesc); the context carries the rank count.
+    if (g->rank != c->rank || (g->num_ranks != 0 && g->num_ranks != c->nranks))
       fail(HGNN_ERR_INTEGRITY, "hgnn_graph_upload: graph rank/num_ranks do not match the context");
     const int64_t nl = g->num_local, nh = g->num_halo, ne = g->num_edges, rows = nl + nh;
     if (nl < 0 || nh < 0 || ne < 0 || rows >= INT32_MAX || ne >= INT32_MAX)

@@ -14,7 +14,8 @@ import pytest
 
 import oracle as O
 from paper_2410_01657_b200 import (Engine, GnnConfig, UninitializedError, build_distributed_graph,
-                                   build_rank_graph, init_params, mp_params)
+                                   build_rank_graph, init_params, load_graph_binary, mp_params,
+                                   save_graph_binary)
 
 pytestmark = pytest.mark.gpu
 
@@ -73,6 +74,23 @@ def test_engine_matches_reference_golden(engine, golden_dir, name):
     assert rel(dx0, z["r0_dx0"]) < BWD_TOL
     assert rel(de0, z["r0_de0"]) < BWD_TOL
     assert grad_rel(grads, z["r0_grads"], cfg) < BWD_TOL
+
+
+def test_graph_loaded_from_hgnngrb1_file_runs_identically(engine, golden_dir, tmp_path):
+    """A graph read back from an HGNNGRB1 file (num_ranks unknown = 0) drives the
+    device path to bitwise the same results as the built graph."""
+    z = np.load(golden_dir / "mp_e2p2_r1_h8.npz")
+    E, p, R, H, M, k, mode, seed = [int(v) for v in z["meta"]]
+    cfg = GnnConfig("g", H, M, k, mode={0: "none", 1: "a2a", 2: "na2a"}[mode])
+    g = build_rank_graph(E, p, 1, 0, "verify")
+    save_graph_binary(g, tmp_path / "r0.bin")
+    h = load_graph_binary(tmp_path / "r0.bin")
+    assert h.num_ranks == 0
+    args = (cfg, z["mp_params"], z["r0_x0"], z["r0_e0"], z["r0_dx"], z["r0_de"])
+    a = run_engine(engine, g, *args)
+    b = run_engine(engine, h, *args)
+    for u, v in zip((a[0], a[1], a[3], a[4], a[5]), (b[0], b[1], b[3], b[4], b[5])):
+        assert u.tobytes() == v.tobytes()
 
 
 CASES = [  # E, p, H, M, k
