@@ -280,6 +280,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     value = wl["unique_nodes"] * M / (ms_max / 1e3)
+    sum_local = g.num_local  # the reference harness's count: coincident copies included (harness.cpp:316-321)
+    if world > 1:
+        t = torch.tensor([float(g.num_local)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        sum_local = int(t.item())
 
     # ---- roofline of the dominant kernel class (live CUDA-event durations)
     per_launch = {c: (t / max(nl_, 1), nl_) for c, (t, nl_) in ktimes.items()}
@@ -334,6 +339,10 @@ def main():
                 "cpu_baseline": cpu, "clocks": clk, "train_step": train,
                 "kernel_share": {c: round(v, 4) for c, v in step_share.items()},
                 "halo_share": round(step_share.get("halo", 0.0), 4), "halo_bytes_per_step_rank0": halo_bytes,
+                "halo_share_basis": ("raw = exposed: pack + NCCL send/recv + sync run on the compute stream "
+                                     "between aggregation and node update (no overlap)"),
+                "sum_local_rows": sum_local,
+                "harness_layer_rows_per_s": sum_local * M / (ms_max / 1e3),
                 "graph_build_s": round(t_graph, 3),
                 "nodes_per_sec_per_iteration": wl["unique_nodes"] / (ms_max / 1e3)}
         print(json.dumps(line), flush=True)
