@@ -8,6 +8,9 @@ Workload (BASELINE.json configs[2] at N=1): 32^3-element GLL box at P=5
 MLP, 4 MP layers, exchange mode na2a. N>1 runs the weak-scaling series of
 configs[4] (~4.2M nodes per GPU: E = 40/50/64 at N = 2/4/8, balanced block
 partition), one GPU per rank, NCCL halo exchange over NVLink.
+--scaling strong keeps one mesh at every N (configs[3]; E = 40 by default,
+--elements 64 for the 33M-node box from N = 4); --mode a2a|none switches the
+halo exchange (configs[4]'s comparison; none = the inconsistent baseline).
 
 metric: MP-layer graph nodes per second, fwd+bwd
         = (unique global nodes) x (MP layers) / (time of one MP-stack fwd+bwd step)
@@ -59,10 +62,18 @@ def choose_elements_for_loading(ranks: int, loading: int, p: int) -> int:
     return best
 
 
-def workload(n_gpus: int):
-    E = 32 if n_gpus == 1 else choose_elements_for_loading(n_gpus, LOADING, P_ORDER)
-    return {"E": E, "p": P_ORDER, "H": HIDDEN, "M": M_LAYERS, "k": K_HIDDEN, "mode": "na2a",
-            "unique_nodes": (E * P_ORDER + 1) ** 3}
+STRONG_E = 40  # strong-scaling default: 201^3 = 8.1M nodes, fits one GPU (configs[3]'s E = 64 fits from N = 4)
+
+
+def workload(n_gpus: int, scaling: str = "weak", mode: str = "na2a"):
+    """weak: configs[2] at N = 1, configs[4]'s ~4.2M nodes per GPU at N > 1.
+    strong: one fixed mesh at every N (configs[3]; E = STRONG_E unless --elements)."""
+    if scaling == "strong":
+        E = STRONG_E
+    else:
+        E = 32 if n_gpus == 1 else choose_elements_for_loading(n_gpus, LOADING, P_ORDER)
+    return {"E": E, "p": P_ORDER, "H": HIDDEN, "M": M_LAYERS, "k": K_HIDDEN, "mode": mode,
+            "scaling": scaling, "unique_nodes": (E * P_ORDER + 1) ** 3}
 
 
 def edge_flops(H, k):
@@ -167,7 +178,10 @@ def cpu_reference_sample(steps: int = 1, E: int = 5):
 def run_reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     n = a.gpus
-    wl = workload(n)
+    wl = workload(n, a.scaling, a.mode)
+    if a.elements:
+        wl["E"] = a.elements
+        wl["unique_nodes"] = (a.elements * P_ORDER + 1) ** 3
     if rank != 0:
         return
     for _ in range(a.warmup if a.warmup < 2 else 1):
@@ -175,7 +189,7 @@ def run_reference_arm(a):
     res = cpu_reference_sample(max(1, a.steps), a.ref_elements)
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": n,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(wl, n), "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind",
                                                                                  "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -207,6 +221,10 @@ def main():
     ap.add_argument("--ref-elements", type=int, default=5)
     ap.add_argument("--elements", type=int, default=0, help="override E (debug)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline / clocks")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: ~4.2M nodes per GPU (configs[4]); strong: one fixed mesh at every N (configs[3])")
+    ap.add_argument("--mode", default="na2a", choices=["na2a", "a2a", "none"],
+                    help="halo exchange mode (configs[4] compares all three; none = the inconsistent baseline)")
     a = ap.parse_args()
     if a.impl == "reference":
         run_reference_arm(a)
@@ -226,7 +244,7 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo", rank=rank, world_size=world)
-    wl = workload(n)
+    wl = workload(n, a.scaling, a.mode)
     if a.elements:
         wl["E"] = a.elements
         wl["unique_nodes"] = (a.elements * P_ORDER + 1) ** 3
@@ -333,7 +351,7 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": a.steps, "warmup": a.warmup,
-                "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "ms_per_step": ms_max, "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic (seeded by global id; random-init weights init_params seed 0)",
                 "config": config_dict(wl, n), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                 "cpu_baseline": cpu, "clocks": clk, "train_step": train,
