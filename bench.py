@@ -225,6 +225,9 @@ def main():
                     help="weak: ~4.2M nodes per GPU (configs[4]); strong: one fixed mesh at every N (configs[3])")
     ap.add_argument("--mode", default="na2a", choices=["na2a", "a2a", "none"],
                     help="halo exchange mode (configs[4] compares all three; none = the inconsistent baseline)")
+    ap.add_argument("--halo-sm-reserve", type=int, default=-1, help="SMs left to the exchange (-1: engine default)")
+    ap.add_argument("--halo-overlap", type=int, default=1, choices=[0, 1],
+                    help="1: forward exchange on a side stream, overlapped with the interior edges (N > 1)")
     a = ap.parse_args()
     if a.impl == "reference":
         run_reference_arm(a)
@@ -264,6 +267,9 @@ def main():
     eng.upload_graph(g)
     eng.configure(cfg)
     eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+    eng.set_option("halo_overlap", a.halo_overlap)
+    if a.halo_sm_reserve >= 0:
+        eng.set_option("halo_sm_reserve", a.halo_sm_reserve)
     eng.synthetic_inputs(seed=1234)
     stream = torch.cuda.ExternalStream(eng.stream_ptr)
 
@@ -357,7 +363,12 @@ def main():
                 "cpu_baseline": cpu, "clocks": clk, "train_step": train,
                 "kernel_share": {c: round(v, 4) for c, v in step_share.items()},
                 "halo_share": round(step_share.get("halo", 0.0), 4), "halo_bytes_per_step_rank0": halo_bytes,
-                "halo_share_basis": ("raw = exposed: pack + NCCL send/recv + sync run on the compute stream "
+                "halo_overlap": bool(a.halo_overlap and n > 1 and wl["mode"] != "none"),
+                "halo_sm_reserve": a.halo_sm_reserve,
+                "halo_share_basis": ("forward: pack + NCCL on a side stream overlapped with the interior edges "
+                                     "(time not exposed); backward: adjoint exchange + sync on the compute stream"
+                                     if a.halo_overlap and n > 1 else
+                                     "raw = exposed: pack + NCCL send/recv + sync run on the compute stream "
                                      "between aggregation and node update (no overlap)"),
                 "sum_local_rows": sum_local,
                 "harness_layer_rows_per_s": sum_local * M / (ms_max / 1e3),

@@ -201,7 +201,15 @@ int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double
 /* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
  *                     0 = SIMT fp32 kernels.
  * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
- *                      0 = SIMT fp32 kernels. */
+ *                      0 = SIMT fp32 kernels.
+ * "halo_overlap":      1 = (default; R > 1, exchange mode set, tcgen05 path) forward:
+ *                      boundary-row edges + aggregates first, then the exchange on
+ *                      a side stream while the interior edges run; backward: the
+ *                      adjoint exchange on the side stream during the interior
+ *                      edges' backward. 0 = the serial schedule. Same results
+ *                      (outputs and adjoints bitwise; weight gradients regrouped).
+ * "halo_sm_reserve":   SMs the overlapped interior launches leave free for the
+ *                      pack / NCCL kernels (0..32). */
 int hgnn_set_option(hgnn_ctx* ctx, const char* key, int64_t value);
 
 /* ---- hardware self-test ----------------------------------------------------- */

@@ -179,7 +179,8 @@ void ensure_buffers(hgnn_ctx* c) {
   plan_mlp(c, false, kNodeInput, c->nl, c->grid_node_b, c->smem_node_b, c->wsm_node_b);
   const int64_t max_grid = std::max<int64_t>({c->grid_edge_b, c->grid_node_b, (int64_t)c->num_sms});
   const int64_t max_par = std::max(c->n_edge_par, c->n_node_par);
-  c->grad_part.alloc(2 * max_grid * max_par);  // tcgen05 backward keeps two partials per CTA
+  // tcgen05 backward: two partials per CTA; the overlapped edge backward runs two launches
+  c->grad_part.alloc(2 * (max_grid + c->num_sms) * max_par);
   const int64_t n_slots = (2 * c->K + 1) * H + c->K;
   c->scratch.alloc(max_grid * n_slots * kMlpThreads);
   if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
@@ -246,13 +247,13 @@ void edges_to_host(hgnn_ctx* c, const float* d, double* h) {
 // --------------------------------------------------------------------------
 // halo exchange (comm.cpp:281-357) over NCCL point-to-point
 // --------------------------------------------------------------------------
-void halo_exchange(hgnn_ctx* c, float* a) {
-  Timed t(c, HGNN_K_HALO);
+void halo_exchange(hgnn_ctx* c, float* a, cudaStream_t st) {
+  Timed t(c, HGNN_K_HALO, st);
   const int64_t H = c->H;
   const int R = c->nranks;
   if (c->mode == HGNN_MODE_NA2A) {
     if (c->n_send > 0) {
-      gather_rows_kernel<<<blocks_for(c->n_send * H / 4), kEwThreads, 0, c->stream>>>(a, c->send_rows.p, nullptr,
+      gather_rows_kernel<<<blocks_for(c->n_send * H / 4), kEwThreads, 0, st>>>(a, c->send_rows.p, nullptr,
                                                                                      c->n_send, (int)H, c->sendbuf.p);
       check_launch(c);
     }
@@ -262,8 +263,8 @@ void halo_exchange(hgnn_ctx* c, float* a) {
         const int64_t cs = c->h_send_off[n + 1] - c->h_send_off[n];
         const int64_t cr = c->h_recv_off[n + 1] - c->h_recv_off[n];
         NCCL_OK(ncclSend(c->sendbuf.p + (int64_t)c->h_send_off[n] * H, (size_t)(cs * H), ncclFloat, c->h_nbr[n],
-                         c->comm, c->stream));
-        NCCL_OK(ncclRecv(a + c->h_recv_base[n] * H, (size_t)(cr * H), ncclFloat, c->h_nbr[n], c->comm, c->stream));
+                         c->comm, st));
+        NCCL_OK(ncclRecv(a + c->h_recv_base[n] * H, (size_t)(cr * H), ncclFloat, c->h_nbr[n], c->comm, st));
         c->halo_bytes += cs * H * (int64_t)sizeof(float);
       }
       NCCL_OK(ncclGroupEnd());
@@ -271,29 +272,29 @@ void halo_exchange(hgnn_ctx* c, float* a) {
   } else if (c->mode == HGNN_MODE_A2A) {
     const int64_t pad = c->max_buffer_rows;
     if (pad == 0 || R == 1) return;
-    CUDA_OK(cudaMemsetAsync(c->sendbuf.p, 0, sizeof(float) * (size_t)(R * pad * H), c->stream));
+    CUDA_OK(cudaMemsetAsync(c->sendbuf.p, 0, sizeof(float) * (size_t)(R * pad * H), st));
     if (c->n_send > 0) {
-      gather_rows_kernel<<<blocks_for(c->n_send * H / 4), kEwThreads, 0, c->stream>>>(
+      gather_rows_kernel<<<blocks_for(c->n_send * H / 4), kEwThreads, 0, st>>>(
           a, c->send_rows.p, c->pos_a2a_send.p, c->n_send, (int)H, c->sendbuf.p);
       check_launch(c);
     }
     NCCL_OK(ncclGroupStart());
     for (int d = 0; d < R; ++d) {
-      NCCL_OK(ncclSend(c->sendbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, c->stream));
-      NCCL_OK(ncclRecv(c->recvbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, c->stream));
+      NCCL_OK(ncclSend(c->sendbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, st));
+      NCCL_OK(ncclRecv(c->recvbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, st));
     }
     NCCL_OK(ncclGroupEnd());
     c->halo_bytes += (int64_t)R * pad * H * (int64_t)sizeof(float);
     if (c->n_recv > 0) {
-      scatter_rows_kernel<<<blocks_for(c->n_recv * H / 4), kEwThreads, 0, c->stream>>>(
+      scatter_rows_kernel<<<blocks_for(c->n_recv * H / 4), kEwThreads, 0, st>>>(
           c->recvbuf.p, c->pos_a2a_recv.p, c->recv_rows.p, c->n_recv, (int)H, a);
       check_launch(c);
     }
   }
 }
 
-void halo_exchange_adjoint(hgnn_ctx* c, float* d_a) {
-  Timed t(c, HGNN_K_HALO);
+void halo_exchange_adjoint(hgnn_ctx* c, float* d_a, cudaStream_t st) {
+  Timed t(c, HGNN_K_HALO, st);
   const int64_t H = c->H;
   const int R = c->nranks;
   const int64_t* acc_pos = nullptr;
@@ -304,9 +305,9 @@ void halo_exchange_adjoint(hgnn_ctx* c, float* d_a) {
         const int64_t cs = c->h_send_off[n + 1] - c->h_send_off[n];
         const int64_t cr = c->h_recv_off[n + 1] - c->h_recv_off[n];
         // halo rows of neighbour n are one contiguous block: sent as they lie
-        NCCL_OK(ncclSend(d_a + c->h_recv_base[n] * H, (size_t)(cr * H), ncclFloat, c->h_nbr[n], c->comm, c->stream));
+        NCCL_OK(ncclSend(d_a + c->h_recv_base[n] * H, (size_t)(cr * H), ncclFloat, c->h_nbr[n], c->comm, st));
         NCCL_OK(ncclRecv(c->recvbuf.p + (int64_t)c->h_send_off[n] * H, (size_t)(cs * H), ncclFloat, c->h_nbr[n],
-                         c->comm, c->stream));
+                         c->comm, st));
         c->halo_bytes += cr * H * (int64_t)sizeof(float);
       }
       NCCL_OK(ncclGroupEnd());
@@ -315,16 +316,16 @@ void halo_exchange_adjoint(hgnn_ctx* c, float* d_a) {
   } else if (c->mode == HGNN_MODE_A2A) {
     const int64_t pad = c->max_buffer_rows;
     if (pad == 0 || R == 1) return;
-    CUDA_OK(cudaMemsetAsync(c->sendbuf.p, 0, sizeof(float) * (size_t)(R * pad * H), c->stream));
+    CUDA_OK(cudaMemsetAsync(c->sendbuf.p, 0, sizeof(float) * (size_t)(R * pad * H), st));
     if (c->n_recv > 0) {
-      gather_rows_kernel<<<blocks_for(c->n_recv * H / 4), kEwThreads, 0, c->stream>>>(
+      gather_rows_kernel<<<blocks_for(c->n_recv * H / 4), kEwThreads, 0, st>>>(
           d_a, c->recv_rows.p, c->pos_a2a_recv.p, c->n_recv, (int)H, c->sendbuf.p);
       check_launch(c);
     }
     NCCL_OK(ncclGroupStart());
     for (int d = 0; d < R; ++d) {
-      NCCL_OK(ncclSend(c->sendbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, c->stream));
-      NCCL_OK(ncclRecv(c->recvbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, c->stream));
+      NCCL_OK(ncclSend(c->sendbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, st));
+      NCCL_OK(ncclRecv(c->recvbuf.p + (int64_t)d * pad * H, (size_t)(pad * H), ncclFloat, d, c->comm, st));
     }
     NCCL_OK(ncclGroupEnd());
     c->halo_bytes += (int64_t)R * pad * H * (int64_t)sizeof(float);
@@ -334,9 +335,9 @@ void halo_exchange_adjoint(hgnn_ctx* c, float* d_a) {
   }
   // the overwritten halo rows contribute nothing upstream (comm.cpp:339-342)
   if (c->nh > 0)
-    CUDA_OK(cudaMemsetAsync(d_a + c->nl * H, 0, sizeof(float) * (size_t)(c->nh * H), c->stream));
+    CUDA_OK(cudaMemsetAsync(d_a + c->nl * H, 0, sizeof(float) * (size_t)(c->nh * H), st));
   if (c->n_acc > 0 && R > 1) {
-    adjoint_accumulate_kernel<<<blocks_for(c->n_acc * H / 4), kEwThreads, 0, c->stream>>>(
+    adjoint_accumulate_kernel<<<blocks_for(c->n_acc * H / 4), kEwThreads, 0, st>>>(
         d_a, c->recvbuf.p, c->acc_rows.p, c->acc_off.p, acc_pos, c->n_acc, (int)H);
     check_launch(c);
   }
@@ -365,23 +366,24 @@ void launch_tc_typed(hgnn_ctx* c, const TcFwdArgs& args) {
   // per launch: the attribute belongs to the current device (cheap host call)
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
   const int64_t pairs = ((args.n_rows + 127) / 128 + 1) / 2;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms - c->sm_reserve));
   k<<<grid, Cfg::THREADS, Cfg::SMEM, c->stream>>>(args);
   check_launch(c);
 }
 
+// Edge mode: slots [s0, s0 + n_rows).
 void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const float* x, const float* e,
-                       const float* a, float* out) {
+                       const float* a, float* out, int64_t s0 = 0) {
   if (n_rows == 0) return;
   const bool edge = mode == kEdgeInput;
   TcFwdArgs args{};
   args.n_rows = n_rows;
-  args.src = c->src.p;
-  args.dst = c->dst.p;
+  args.src = c->src.p + s0;
+  args.dst = c->dst.p + s0;
   args.x = x;
-  args.e_in = e;
+  args.e_in = e ? e + s0 * c->H : nullptr;
   args.a = a;
-  args.out = out;
+  args.out = out + s0 * c->H;
   args.chunks = c->chunks.p + c->chunk_off[(size_t)(2 * m + (edge ? 0 : 1))];
   args.params = layer_params(c, m, edge).p;
   args.k = (int)c->K;
@@ -399,7 +401,7 @@ bool use_tc_bwd(const hgnn_ctx* c) { return c->bwd_impl == 1 && c->H == 64; }
 
 int tc_bwd_grid(const hgnn_ctx* c, int64_t n_rows) {
   const int64_t pairs = ((n_rows + 127) / 128 + 1) / 2;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms - c->sm_reserve));
 }
 
 // Returns the grid used (rows of grad_part written).
@@ -421,6 +423,24 @@ int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
   return grid;
 }
 
+// node update on local rows (model.cpp:260-264)
+void node_forward(hgnn_ctx* c, int64_t m, const float* x, const float* a, float* x2) {
+  const int64_t H = c->H;
+  Timed t(c, HGNN_K_NODE_FWD);
+  if (c->nh > 0) CUDA_OK(cudaMemsetAsync(x2 + c->nl * H, 0, sizeof(float) * (size_t)(c->nh * H), c->stream));
+  if (use_tc(c)) {
+    launch_tc_forward(c, kNodeInput, m, c->nl, x, nullptr, a, x2);
+  } else {
+    MlpRowArgs args{};
+    args.n_rows = c->nl;
+    args.x = x;
+    args.a = a;
+    args.out = x2;
+    launch_mlp(c, true, kNodeInput, args, layer_params(c, m, false));
+  }
+}
+
+
 void layer_forward(hgnn_ctx* c, int64_t m) {
   const int64_t H = c->H;
   float* x = c->xs[m]->p;
@@ -428,6 +448,46 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   float* e2 = c->es[m + 1]->p;
   float* a = c->as[m]->p;
   float* x2 = c->xs[m + 1]->p;
+  if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && c->comm && c->n_rows_bnd > 0 && use_tc(c)) {
+    // Overlapped schedule, same results: boundary-row edges + aggregates,
+    // then the exchange on the side stream while the interior edges run on
+    // all but halo_sm_reserve SMs (left to the pack and NCCL kernels).
+    {
+      Timed t(c, HGNN_K_EDGE_FWD);
+      launch_tc_forward(c, kEdgeInput, m, c->ne_bnd, x, e, nullptr, e2, 0);
+    }
+    {
+      Timed t(c, HGNN_K_AGG);
+      aggregate_kernel<<<blocks_for(c->n_rows_bnd * H / 4), kEwThreads, 0, c->stream>>>(
+          e2, c->inv.p, c->seg_beg.p, c->seg_end.p, c->rows_bnd.p, c->n_rows_bnd, (int)H, a);
+      check_launch(c);
+    }
+    CUDA_OK(cudaEventRecord(c->ev_bnd, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_bnd, 0));
+    halo_exchange(c, a, c->side);
+    CUDA_OK(cudaEventRecord(c->ev_halo, c->side));
+    {
+      Timed t(c, HGNN_K_EDGE_FWD);
+      c->sm_reserve = c->halo_sm_reserve;
+      launch_tc_forward(c, kEdgeInput, m, c->ne - c->ne_bnd, x, e, nullptr, e2, c->ne_bnd);
+      c->sm_reserve = 0;
+    }
+    if (c->n_rows_int > 0) {
+      Timed t(c, HGNN_K_AGG);
+      aggregate_kernel<<<blocks_for(c->n_rows_int * H / 4), kEwThreads, 0, c->stream>>>(
+          e2, c->inv.p, c->seg_beg.p, c->seg_end.p, c->rows_int.p, c->n_rows_int, (int)H, a);
+      check_launch(c);
+    }
+    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    if (c->n_sync > 0) {
+      Timed t(c, HGNN_K_HALO);
+      sync_kernel<<<blocks_for(c->n_sync * H / 4), kEwThreads, 0, c->stream>>>(a, c->sync_local.p, c->sync_off.p,
+                                                                              c->sync_slots.p, c->n_sync, (int)H);
+      check_launch(c);
+    }
+    node_forward(c, m, x, a, x2);
+    return;
+  }
   {  // edge update (model.cpp:233-235)
     Timed t(c, HGNN_K_EDGE_FWD);
     if (use_tc(c)) {
@@ -445,12 +505,12 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   }
   {  // degree-scaled aggregation (model.cpp:237-240)
     Timed t(c, HGNN_K_AGG);
-    aggregate_kernel<<<blocks_for(c->rows * H / 4), kEwThreads, 0, c->stream>>>(e2, c->inv.p, c->in_off.p, c->rows,
-                                                                               (int)H, a);
+    aggregate_kernel<<<blocks_for(c->rows * H / 4), kEwThreads, 0, c->stream>>>(
+        e2, c->inv.p, c->seg_beg.p, c->seg_end.p, nullptr, c->rows, (int)H, a);
     check_launch(c);
   }
   if (c->mode != HGNN_MODE_NONE) {  // exchange + synchronisation (model.cpp:243-257)
-    halo_exchange(c, a);
+    halo_exchange(c, a, c->stream);
     if (c->n_sync > 0) {
       Timed t(c, HGNN_K_HALO);
       sync_kernel<<<blocks_for(c->n_sync * H / 4), kEwThreads, 0, c->stream>>>(a, c->sync_local.p, c->sync_off.p,
@@ -458,20 +518,7 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
       check_launch(c);
     }
   }
-  {  // node update on local rows (model.cpp:260-264)
-    Timed t(c, HGNN_K_NODE_FWD);
-    if (c->nh > 0) CUDA_OK(cudaMemsetAsync(x2 + c->nl * H, 0, sizeof(float) * (size_t)(c->nh * H), c->stream));
-    if (use_tc(c)) {
-      launch_tc_forward(c, kNodeInput, m, c->nl, x, nullptr, a, x2);
-    } else {
-      MlpRowArgs args{};
-      args.n_rows = c->nl;
-      args.x = x;
-      args.a = a;
-      args.out = x2;
-      launch_mlp(c, true, kNodeInput, args, layer_params(c, m, false));
-    }
-  }
+  node_forward(c, m, x, a, x2);
 }
 
 void reduce_grads(hgnn_ctx* c, int grid, int64_t n_par, double* out) {
@@ -522,6 +569,59 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       if (c->nl > 0) reduce_grads(c, c->grid_node_b, c->n_node_par, c->grads.p + goff + c->n_edge_par);
     }
   }
+  if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && c->comm && c->n_rows_bnd > 0 &&
+      use_tc_bwd(c)) {
+    // Overlapped schedule: sync adjoint, then the adjoint exchange on the side
+    // stream while the interior edges (receivers whose d_a the exchange does
+    // not touch) run their backward; the boundary edges follow the exchange.
+    if (c->n_sync > 0) {
+      Timed t(c, HGNN_K_HALO);
+      sync_adjoint_kernel<<<blocks_for(c->n_sync * H / 4), kEwThreads, 0, c->stream>>>(
+          c->d_a.p, c->sync_local.p, c->sync_off.p, c->sync_slots.p, c->n_sync, (int)H);
+      check_launch(c);
+    }
+    CUDA_OK(cudaEventRecord(c->ev_bnd, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_bnd, 0));
+    halo_exchange_adjoint(c, c->d_a.p, c->side);
+    CUDA_OK(cudaEventRecord(c->ev_halo, c->side));
+    const int64_t n_int = c->ne - c->ne_bnd;
+    c->sm_reserve = c->halo_sm_reserve;
+    const int g1 = n_int > 0 ? tc_bwd_grid(c, n_int) : 0;
+    c->sm_reserve = 0;
+    const int g2 = c->ne_bnd > 0 ? tc_bwd_grid(c, c->ne_bnd) : 0;
+    auto edge_args = [&](int64_t s0, int64_t n, float* part) {
+      TcBwdArgs args{};
+      args.n_rows = n;
+      args.src = c->src.p + s0;
+      args.dst = c->dst.p + s0;
+      args.x = x;
+      args.e_in = e + s0 * H;
+      args.inv_deg = c->inv.p + s0;
+      args.d_a = c->d_a.p;
+      args.de_io = c->de.p + s0 * H;
+      args.d_src = c->dsrc.p + s0 * H;
+      args.d_dst = c->ddst.p + s0 * H;
+      args.grad_partial = part;
+      return args;
+    };
+    {
+      Timed t(c, HGNN_K_EDGE_BWD);
+      CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * (g1 + g2) * c->n_edge_par),
+                              c->stream));
+      if (n_int > 0) {
+        c->sm_reserve = c->halo_sm_reserve;
+        launch_tc_backward(c, kEdgeInput, m, edge_args(c->ne_bnd, n_int, c->grad_part.p));
+        c->sm_reserve = 0;
+      }
+    }
+    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    {
+      Timed t(c, HGNN_K_EDGE_BWD);
+      if (c->ne_bnd > 0)
+        launch_tc_backward(c, kEdgeInput, m, edge_args(0, c->ne_bnd, c->grad_part.p + 2 * g1 * c->n_edge_par));
+      reduce_grads(c, 2 * (g1 + g2), c->n_edge_par, c->grads.p + goff);
+    }
+  } else {
   if (c->mode != HGNN_MODE_NONE) {  // sync + exchange adjoints (model.cpp:343-351)
     if (c->n_sync > 0) {
       Timed t(c, HGNN_K_HALO);
@@ -529,7 +629,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
           c->d_a.p, c->sync_local.p, c->sync_off.p, c->sync_slots.p, c->n_sync, (int)H);
       check_launch(c);
     }
-    halo_exchange_adjoint(c, c->d_a.p);
+    halo_exchange_adjoint(c, c->d_a.p, c->stream);
   }
   {  // aggregation + edge update backward (model.cpp:353-375)
     Timed t(c, HGNN_K_EDGE_BWD);
@@ -572,10 +672,11 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       if (c->ne > 0) reduce_grads(c, c->grid_edge_b, c->n_edge_par, c->grads.p + goff);
     }
   }
+  }  // serial schedule
   {  // input-node adjoint (model.cpp:378-386)
     Timed t(c, HGNN_K_DX);
     dx_gather_kernel<<<blocks_for(c->rows * H / 4), kEwThreads, 0, c->stream>>>(
-        c->dsrc.p, c->ddst.p, c->dxn.p, c->in_off.p, c->twin.p, c->rows, c->nl, (int)H, c->dx.p);
+        c->dsrc.p, c->ddst.p, c->dxn.p, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, (int)H, c->dx.p);
     check_launch(c);
   }
 }
@@ -640,6 +741,9 @@ int hgnn_ctx_create(int device, int32_t rank, int32_t nranks, const uint8_t* uid
                                              std::to_string(major));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
     if (nranks > 1) {
       if (!uid) fail(HGNN_ERR_CONFIG, "hgnn_ctx_create: nccl unique id required for num_ranks > 1");
       ncclUniqueId id;
@@ -661,6 +765,9 @@ int hgnn_ctx_destroy(hgnn_ctx* c) {
         cudaEventDestroy(p.b);
       }
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    if (c->side) cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->stream);
     delete c;
   });
@@ -680,15 +787,47 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
     if (nl < 0 || nh < 0 || ne < 0 || rows >= INT32_MAX || ne >= INT32_MAX)
       fail(HGNN_ERR_SHAPE, "hgnn_graph_upload: sizes out of range");
     if (ne % 2) fail(HGNN_ERR_INTEGRITY, "directed edges must come in twin pairs (graph.cpp:107-110)");
-    // receiver-sorted slots = in-CSR order; twin slots via the e^1 pairing
+    // Slots: receiver segments in in-CSR order (each segment keeps the
+    // reference's in-edge order, so every per-row sum is unchanged); with
+    // R > 1 the boundary rows' segments (rows the exchange packs) come first.
+    // Twin slots via the e^1 pairing.
+    if (g->in_offsets[0] != 0 || g->in_offsets[rows] != ne) fail(HGNN_ERR_INTEGRITY, "in_offsets do not span N_e");
+    const int nn0 = g->num_neighbors;
+    const int64_t n_send0 = nn0 > 0 ? g->send_offsets[nn0] : 0;
+    std::vector<uint8_t> bnd((size_t)rows, 0);
+    for (int64_t i = nl; i < rows; ++i) bnd[(size_t)i] = 1;  // halo rows: no in-edges, zeroed before the receive
+    for (int64_t t = 0; t < n_send0; ++t) {
+      const int32_t r = g->send_rows[t];
+      if (r < 0 || r >= nl) fail(HGNN_ERR_INTEGRITY, "send rows must be local rows");
+      bnd[(size_t)r] = 1;
+    }
+    const bool split = c->nranks > 1 && n_send0 > 0;
+    std::vector<int32_t> new_of_old((size_t)ne), seg_b((size_t)rows), seg_e((size_t)rows), rb, ri;
+    int32_t next = 0;
+    auto place = [&](int64_t i) {
+      seg_b[(size_t)i] = next;
+      for (int32_t p = g->in_offsets[i]; p < g->in_offsets[i + 1]; ++p) new_of_old[(size_t)p] = next++;
+      seg_e[(size_t)i] = next;
+    };
+    for (int64_t i = 0; i < rows; ++i)
+      if (!split || bnd[(size_t)i]) {
+        place(i);
+        rb.push_back((int32_t)i);
+      }
+    const int64_t ne_bnd = split ? next : ne;
+    if (split)
+      for (int64_t i = 0; i < rows; ++i)
+        if (!bnd[(size_t)i]) {
+          place(i);
+          ri.push_back((int32_t)i);
+        }
     std::vector<int32_t> slot_of((size_t)ne), src_s((size_t)ne), dst_s((size_t)ne), twin((size_t)ne);
     std::vector<float> inv_s((size_t)ne);
-    if (g->in_offsets[0] != 0 || g->in_offsets[rows] != ne) fail(HGNN_ERR_INTEGRITY, "in_offsets do not span N_e");
     for (int64_t i = 0; i < rows; ++i)
       for (int32_t p = g->in_offsets[i]; p < g->in_offsets[i + 1]; ++p) {
         const int32_t e = g->in_edges[p];
         if (e < 0 || e >= ne || g->edge_dst[e] != i) fail(HGNN_ERR_INTEGRITY, "in-CSR inconsistent with edge_dst");
-        slot_of[(size_t)e] = p;
+        slot_of[(size_t)e] = new_of_old[(size_t)p];
       }
     for (int64_t p = 0; p < ne; ++p) {
       const int32_t e = g->in_edges[p];
@@ -696,10 +835,11 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
       if (s < 0 || s >= nl || d < 0 || d >= nl) fail(HGNN_ERR_INTEGRITY, "edges must not reference halo rows");
       const int32_t t = e ^ 1;
       if (g->edge_src[t] != d || g->edge_dst[t] != s) fail(HGNN_ERR_INTEGRITY, "edge e^1 is not the twin of e");
-      src_s[(size_t)p] = s;
-      dst_s[(size_t)p] = d;
-      inv_s[(size_t)p] = (float)g->edge_inv_degree[e];
-      twin[(size_t)p] = slot_of[(size_t)t];
+      const size_t q = (size_t)new_of_old[(size_t)p];
+      src_s[q] = s;
+      dst_s[q] = d;
+      inv_s[q] = (float)g->edge_inv_degree[e];
+      twin[q] = slot_of[(size_t)t];
     }
     c->nl = nl;
     c->nh = nh;
@@ -712,7 +852,13 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
     c->slot_of.upload(slot_of.data(), ne, c->stream);
     c->inv.upload(inv_s.data(), ne, c->stream);
     if (g->node_inv_degree) c->node_inv.upload(g->node_inv_degree, nl, c->stream);
-    c->in_off.upload(g->in_offsets, rows + 1, c->stream);
+    c->seg_beg.upload(seg_b.data(), rows, c->stream);
+    c->seg_end.upload(seg_e.data(), rows, c->stream);
+    c->ne_bnd = ne_bnd;
+    c->n_rows_bnd = split ? (int64_t)rb.size() : 0;
+    c->n_rows_int = split ? (int64_t)ri.size() : 0;
+    c->rows_bnd.upload(rb.data(), c->n_rows_bnd, c->stream);
+    c->rows_int.upload(ri.data(), c->n_rows_int, c->stream);
     std::vector<int64_t> gids(g->global_ids, g->global_ids + rows);
     c->gid.upload(gids.data(), rows, c->stream);
     // halo map
@@ -990,6 +1136,12 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       c->prof.alloc(4 * kProfCount);
       CUDA_OK(cudaMemsetAsync(c->prof.p, 0, sizeof(unsigned long long) * 4 * kProfCount, c->stream));
       c->prof_on = value != 0;
+    } else if (k == "halo_overlap") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "halo_overlap: 0 (serial) or 1 (exchange overlapped)");
+      c->halo_overlap = (int)value;
+    } else if (k == "halo_sm_reserve") {
+      if (value < 0 || value > 32) fail(HGNN_ERR_CONFIG, "halo_sm_reserve: 0..32 SMs");
+      c->halo_sm_reserve = (int)value;
     } else if (k == "mlp_backward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
       c->bwd_impl = (int)value;

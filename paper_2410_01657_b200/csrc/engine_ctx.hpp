@@ -75,7 +75,18 @@ struct hgnn_ctx {
 
   // graph
   int64_t nl = 0, nh = 0, rows = 0, ne = 0, max_buffer_rows = 0;
-  hgnn_b200::DevBuf<int32_t> src, dst, in_off, twin, slot_of;
+  hgnn_b200::DevBuf<int32_t> src, dst, twin, slot_of;
+  // Slot order: receiver-sorted, and for R > 1 the segments of the boundary
+  // rows (rows packed by the halo exchange) first, so the overlapped forward
+  // can finish them, start the exchange and run the interior edges meanwhile.
+  // Row i's in-edges are slots [seg_beg[i], seg_end[i]) in in-CSR order.
+  hgnn_b200::DevBuf<int32_t> seg_beg, seg_end, rows_bnd, rows_int;
+  int64_t ne_bnd = 0, n_rows_bnd = 0, n_rows_int = 0;
+  int halo_overlap = 1;   // option "halo_overlap": exchange on `side` overlapped with the interior edges
+  int halo_sm_reserve = 0;  // option "halo_sm_reserve": SMs the interior edge launches leave to pack / NCCL
+  int sm_reserve = 0;       // the reserve in force for the launch being issued
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   hgnn_b200::DevBuf<float> inv;
   hgnn_b200::DevBuf<int64_t> gid;
   // halo
@@ -147,7 +158,7 @@ inline unsigned blocks_for(int64_t n, int threads = kEwThreads) {
 struct Timed {
   hgnn_ctx* c;
   int cls;
-  Timed(hgnn_ctx* ctx, int k) : c(ctx), cls(k) {
+  Timed(hgnn_ctx* ctx, int k, cudaStream_t s = nullptr) : c(ctx), cls(k), st(s ? s : ctx->stream) {
     if (!c->timing) return;
     auto& v = c->ev[cls];
     if (c->ev_used[cls] == v.size()) {
@@ -156,15 +167,16 @@ struct Timed {
       CUDA_OK(cudaEventCreate(&p.b));
       v.push_back(p);
     }
-    CUDA_OK(cudaEventRecord(v[c->ev_used[cls]].a, c->stream));
+    CUDA_OK(cudaEventRecord(v[c->ev_used[cls]].a, st));
   }
   ~Timed() { stop(); }
   void stop() {
     if (!c->timing || done) return;
     done = true;
-    cudaEventRecord(c->ev[cls][c->ev_used[cls]].b, c->stream);
+    cudaEventRecord(c->ev[cls][c->ev_used[cls]].b, st);
     c->ev_used[cls] += 1;
   }
+  cudaStream_t st;
   bool done = false;
 };
 

@@ -25,16 +25,20 @@ __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
 
 // a[i] = sum_{p in [off[i], off[i+1])} inv[p] * e[p]   (scatter_rows_csr,
 // kernels.cpp:174-186, applied at model.cpp:238-240). Halo rows: empty -> 0.
+// Rows row_list[0..n) (all rows when row_list is null); row i's in-edges are
+// slots [beg[i], end[i]) in in-CSR order.
 __global__ void aggregate_kernel(const float* __restrict__ e, const float* __restrict__ inv,
-                                 const int32_t* __restrict__ off, int64_t rows, int H, float* __restrict__ a) {
+                                 const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
+                                 const int32_t* __restrict__ row_list, int64_t n, int H, float* __restrict__ a) {
   const int q = H / 4;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= rows * q) return;
-  const int64_t i = tid / q;
+  if (tid >= n * q) return;
+  const int64_t t = tid / q;
+  const int64_t i = row_list ? (int64_t)__ldg(row_list + t) : t;
   const int c = (int)(tid % q);
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int32_t p1 = __ldg(off + i + 1);
-  for (int32_t p = __ldg(off + i); p < p1; ++p)
+  const int32_t p1 = __ldg(end + i);
+  for (int32_t p = __ldg(beg + i); p < p1; ++p)
     s = f4_fma(__ldg(inv + p), __ldg(reinterpret_cast<const float4*>(e + (int64_t)p * H) + c), s);
   reinterpret_cast<float4*>(a + i * H)[c] = s;
 }
@@ -125,8 +129,8 @@ __global__ void adjoint_accumulate_kernel(float* __restrict__ d_a, const float* 
 // same ascending order), plus the in-CSR sum of d_x_dst, plus the node-update
 // adjoint on local rows.
 __global__ void dx_gather_kernel(const float* __restrict__ d_src, const float* __restrict__ d_dst,
-                                 const float* __restrict__ dx_node, const int32_t* __restrict__ off,
-                                 const int32_t* __restrict__ twin, int64_t rows, int64_t n_local, int H,
+                                 const float* __restrict__ dx_node, const int32_t* __restrict__ beg,
+                                 const int32_t* __restrict__ end, const int32_t* __restrict__ twin, int64_t rows, int64_t n_local, int H,
                                  float* __restrict__ dx) {
   const int q = H / 4;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -134,8 +138,8 @@ __global__ void dx_gather_kernel(const float* __restrict__ d_src, const float* _
   const int64_t i = tid / q;
   const int c = (int)(tid % q);
   float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s1;
-  const int32_t p1 = __ldg(off + i + 1);
-  for (int32_t p = __ldg(off + i); p < p1; ++p) {
+  const int32_t p1 = __ldg(end + i);
+  for (int32_t p = __ldg(beg + i); p < p1; ++p) {
     s1 = f4_add(s1, __ldg(reinterpret_cast<const float4*>(d_src + (int64_t)__ldg(twin + p) * H) + c));
     s2 = f4_add(s2, __ldg(reinterpret_cast<const float4*>(d_dst + (int64_t)p * H) + c));
   }

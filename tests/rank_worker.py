@@ -56,7 +56,11 @@ def main():
     a_sync0 = eng.trace(0, "a_sync")
     dx0, de0, grads = eng.nmp_backward(dx)
     x_out2 = eng.nmp_forward(x0, e0)
+    eng.set_option("halo_overlap", 0)  # the serial schedule (exchange between aggregation and node update)
+    x_ser, e_ser = eng.nmp_forward(x0, e0, want_e=True)
+    dx0_s, de0_s, grads_s = eng.nmp_backward(dx)
     np.savez(a.out, x_out=x_out, e_out=e_out, a_sync0=a_sync0, dx0=dx0, de0=de0, grads=grads, x_out2=x_out2,
+             x_serial=x_ser, e_serial=e_ser, dx0_serial=dx0_s, de0_serial=de0_s, grads_serial=grads_s,
              halo_bytes=eng.halo_bytes())
     eng.close()
 
