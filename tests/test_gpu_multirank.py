@@ -67,7 +67,8 @@ def by_gid(graphs, ys):
 
 
 @pytest.mark.parametrize("R,E,p,H,M,k,mode", [(2, 2, 3, 32, 2, 5, "na2a"), (2, 4, 2, 64, 2, 2, "a2a"),
-                                              (2, 4, 3, 16, 3, 2, "none")])
+                                              (2, 4, 3, 16, 3, 2, "none"), (4, 4, 2, 64, 2, 2, "na2a"),
+                                              (4, 4, 3, 32, 2, 3, "a2a")])
 def test_two_gpu_parity_and_consistency(gpus, R, E, p, H, M, k, mode):
     if gpus < R:
         pytest.skip(f"needs {R} GPUs")
