@@ -335,6 +335,22 @@ def main():
                 "pipe": ("tcgen05 kind::tf32 3xTF32 (3 tensor products per algorithmic product; the backward "
                          "kernel also recomputes the forward: algorithmic flops exclude both)")}
 
+    # ---- HBM-bound kernels: algorithmic bytes per step / live kernel time per step
+    hbm_peak = peaks.get("hbm_gbs") or 7700.0
+    per_layer_bytes = {
+        # e' rows + 1/d per in-edge read, a row written, segment bounds
+        "aggregate": g.num_edges * (H * 4 + 4) + g.rows * (H * 4 + 8),
+        # d_src (twin slot) + d_dst rows and the twin index per in-edge, dx_node read, dx written
+        "dx_gather": g.num_edges * (2 * H * 4 + 4) + g.num_local * H * 4 + g.rows * (H * 4 + 8),
+    }
+    hbm = {}
+    for cls_, b in per_layer_bytes.items():
+        t_step = ktimes[cls_][0] / a.steps
+        if t_step > 0:
+            gbs = b * M / (t_step / 1e3) / 1e9
+            hbm[cls_] = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                         "bytes_per_step": b * M, "ms_per_step": t_step}
+
     # ---- e2e through the public C-ABI with host buffers
     e2e = None
     if not a.no_e2e and not a.profile:
@@ -360,7 +376,7 @@ def main():
                 "ms_per_step": ms_max, "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic (seeded by global id; random-init weights init_params seed 0)",
                 "config": config_dict(wl, n), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
-                "cpu_baseline": cpu, "clocks": clk, "train_step": train,
+                "cpu_baseline": cpu, "clocks": clk, "train_step": train, "hbm_kernels": hbm,
                 "kernel_share": {c: round(v, 4) for c, v in step_share.items()},
                 "halo_share": round(step_share.get("halo", 0.0), 4), "halo_bytes_per_step_rank0": halo_bytes,
                 "halo_overlap": bool(a.halo_overlap and n > 1 and wl["mode"] != "none"),
