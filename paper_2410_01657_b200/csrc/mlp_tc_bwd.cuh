@@ -58,6 +58,8 @@ struct TcBwdCfg {
   static constexpr size_t SMEM = OFF_BIAS + 18 * 64 * 4 + 1024;
 };
 
+constexpr bool kDiscardScratch = true;  // see the backward walk
+
 struct TcBwdArgs {
   int64_t n_rows;
   const int32_t* src;
@@ -500,6 +502,16 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
             dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
             dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
+          }
+          if (kDiscardScratch) {
+            // t_l and inv_std of this tile are dead: drop their L2 lines instead
+            // of letting them be written back (8 rows of one q per 128-B line)
+            __syncwarp();
+            if ((trow & 7) == 0) {
+#pragma unroll 4
+              for (int q = 0; q < 16; ++q) ptx::discard_l2_line(st + q * 128);
+            }
+            if ((trow & 31) == 0) ptx::discard_l2_line(scr_inv + (l - 1) * 128 + trow);
           }
           if (PROF) pf[6] += (unsigned long long)(clock64() - tl0);
         }
