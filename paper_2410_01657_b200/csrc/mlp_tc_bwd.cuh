@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-          ptx::st_hint(st + q * 128, make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]), keep);
+          st[q * 128] = make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
         scr_inv[(l - 1) * 128 + trow] = inv_std;
 #pragma unroll
         for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
