@@ -126,6 +126,19 @@ int hgnn_nccl_unique_id(uint8_t out[128]);
 
 /* device: CUDA ordinal; uid may be NULL when num_ranks == 1. */
 int hgnn_ctx_create(int device, int32_t rank, int32_t num_ranks, const uint8_t* nccl_uid, hgnn_ctx** out);
+
+/* In-process rank group: the reference's RankRuntime (comm.cpp:35-93) — R
+ * ranks driven by R host threads of one process, each with its own context,
+ * on one GPU or several. Exchanges and all-reduces rendezvous on the host with
+ * the reference's rule (same collective, same order on every rank; a mismatch
+ * poisons the group and every rank gets HGNN_ERR_COLLECTIVE, comm.cpp:168-208)
+ * and move data with device-to-device copies; a rank that does not arrive
+ * within the timeout (default 120 s) fails its peers instead of hanging them. */
+typedef struct hgnn_local_group hgnn_local_group;
+int hgnn_local_group_create(int32_t num_ranks, hgnn_local_group** out);
+int hgnn_local_group_destroy(hgnn_local_group* group); /* after every member context is destroyed */
+int hgnn_local_group_set_timeout(hgnn_local_group* group, int64_t timeout_ms);
+int hgnn_ctx_create_local(int device, int32_t rank, hgnn_local_group* group, hgnn_ctx** out);
 int hgnn_ctx_destroy(hgnn_ctx* ctx);
 /* cudaStream_t of the compute stream, as an opaque pointer (for event timing). */
 void* hgnn_ctx_stream(hgnn_ctx* ctx);
@@ -211,20 +224,6 @@ int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double
  * "halo_sm_reserve":   SMs the overlapped interior launches leave free for the
  *                      pack / NCCL kernels (0..32). */
 int hgnn_set_option(hgnn_ctx* ctx, const char* key, int64_t value);
-
-/* ---- hardware self-test ----------------------------------------------------- */
-/* One 128 x 128 x 32 tcgen05 kind::tf32 MMA on caller data (A 128x32, B 32x128,
- * row-major fp32; D 128x128). mode 0: A in TMEM + B K-major (forward / dX path),
- * 1: A and B MN-major in shared memory (dW path), 2: both K-major in shared memory. */
-int hgnn_selftest_mma(int mode, const float* A, const float* B, float* D);
-/* MMA issue-rate microbenchmark (debug aid): `blocks` CTAs each issue iters x 24
- * kind::tf32 M=128 K=8 MMAs with N = n (A from TMEM if ts, else SMEM) into nd
- * round-robin accumulators (nd * n <= 256 columns); cycles_out[b] = clock64
- * cycles of CTA b from first issue to completion. */
-int hgnn_bench_mma(int iters, int n, int ts, int nd, int blocks, uint64_t* cycles_out);
-/* SFU / FMA throughput microbenchmark (debug aid): kind 0 ex2.approx, 1 fma,
- * 2 rsqrt.approx; threads x 8 independent chains x iters operations per block. */
-int hgnn_bench_alu(int kind, int iters, int threads, int blocks, uint64_t* cycles_out);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* When enabled, every launch of the listed kernel classes is bracketed by CUDA

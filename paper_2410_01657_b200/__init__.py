@@ -6,14 +6,14 @@ CPU fallback: importing this package fails if the native library is absent.
 """
 from ._native import (CollectiveError, ConfigError, DeviceError, Error, IntegrityError, IoError,
                       OptimizerError, PartitionError, ShapeError, SizeError, UninitializedError, lib_path)
-from .engine import Engine, nccl_unique_id
+from .engine import Engine, LocalGroup, nccl_unique_id
 from .graph import (RankGraph, balanced_factors, build_distributed_graph, build_rank_graph, load_graph_binary,
                     save_graph_binary)
 from .params import (GnnConfig, init_params, model_slices, mp_layer_slices, mp_param_range, mp_params,
                      param_count)
 
 __all__ = [
-    "Engine", "nccl_unique_id", "RankGraph", "build_rank_graph", "build_distributed_graph", "balanced_factors",
+    "Engine", "LocalGroup", "nccl_unique_id", "RankGraph", "build_rank_graph", "build_distributed_graph", "balanced_factors",
     "load_graph_binary", "save_graph_binary",
     "GnnConfig", "init_params", "mp_params", "mp_param_range", "mp_layer_slices", "model_slices", "param_count",
     "lib_path",

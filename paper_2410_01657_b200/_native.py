@@ -126,6 +126,10 @@ def _load() -> C.CDLL:
         "hgnn_device_count": (C.c_int, []),
         "hgnn_nccl_unique_id": (C.c_int, [u8p]),
         "hgnn_ctx_create": (C.c_int, [C.c_int, C.c_int32, C.c_int32, u8p, C.POINTER(vp)]),
+        "hgnn_local_group_create": (C.c_int, [C.c_int32, C.POINTER(vp)]),
+        "hgnn_local_group_destroy": (C.c_int, [vp]),
+        "hgnn_local_group_set_timeout": (C.c_int, [vp, C.c_int64]),
+        "hgnn_ctx_create_local": (C.c_int, [C.c_int, C.c_int32, vp, C.POINTER(vp)]),
         "hgnn_ctx_destroy": (C.c_int, [vp]),
         "hgnn_ctx_stream": (vp, [vp]),
         "hgnn_graph_upload": (C.c_int, [vp, C.POINTER(GraphDesc)]),
@@ -139,10 +143,7 @@ def _load() -> C.CDLL:
         "hgnn_mp_step_device": (C.c_int, [vp]),
         "hgnn_get_grads": (C.c_int, [vp, f64p]),
         "hgnn_set_option": (C.c_int, [vp, C.c_char_p, C.c_int64]),
-        "hgnn_selftest_mma": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
         "hgnn_debug_profile": (C.c_int, [vp, C.c_void_p]),
-        "hgnn_bench_mma": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
-        "hgnn_bench_alu": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
         "hgnn_model_configure": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64]),
         "hgnn_model_param_count": (C.c_int64, [vp]),
         "hgnn_model_params_upload": (C.c_int, [vp, f64p, C.c_int64]),
@@ -166,10 +167,11 @@ LIB = _load()
 EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_graph_view", "hgnn_graph_save_binary",
             "hgnn_graph_load_binary", "hgnn_balanced_factors",
             "hgnn_param_count", "hgnn_init_params", "hgnn_mp_param_range", "hgnn_device_count", "hgnn_nccl_unique_id",
-            "hgnn_ctx_create", "hgnn_ctx_destroy", "hgnn_ctx_stream", "hgnn_graph_upload", "hgnn_configure",
+            "hgnn_ctx_create", "hgnn_local_group_create", "hgnn_local_group_destroy", "hgnn_local_group_set_timeout",
+            "hgnn_ctx_create_local", "hgnn_ctx_destroy", "hgnn_ctx_stream", "hgnn_graph_upload", "hgnn_configure",
             "hgnn_params_upload", "hgnn_mp_forward", "hgnn_mp_backward", "hgnn_get_trace",
             "hgnn_synthetic_inputs", "hgnn_set_inputs", "hgnn_mp_step_device", "hgnn_get_grads",
-            "hgnn_set_option", "hgnn_selftest_mma", "hgnn_bench_mma", "hgnn_bench_alu", "hgnn_model_configure", "hgnn_model_param_count",
+            "hgnn_set_option", "hgnn_model_configure", "hgnn_model_param_count",
             "hgnn_model_params_upload", "hgnn_model_params_download", "hgnn_model_set_data", "hgnn_compute_gradients",
             "hgnn_train_step", "hgnn_debug_profile", "hgnn_kernel_timing", "hgnn_kernel_time", "hgnn_launch_count", "hgnn_halo_bytes"]
 
@@ -182,3 +184,12 @@ def check(status: int) -> None:
 
 def lib_path() -> str:
     return os.fspath(_LIB_PATH)
+
+
+def debug_lib() -> C.CDLL:
+    """lib/libhgnn_b200_debug.so: tcgen05 self-tests and microbenchmarks (scripts/dbg_*.py)."""
+    lib = C.CDLL(os.fspath(_LIB_PATH.parent / "libhgnn_b200_debug.so"))
+    lib.hgnn_selftest_mma.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.hgnn_bench_mma.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    lib.hgnn_bench_alu.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    return lib

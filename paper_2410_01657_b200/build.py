@@ -24,13 +24,15 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 OBJ_DIR = PKG / "build"
 LIB = LIB_DIR / "libhgnn_b200.so"
+DEBUG_LIB = LIB_DIR / "libhgnn_b200_debug.so"  # tcgen05 self-tests / microbenchmarks (scripts/dbg_*.py only)
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-Xcompiler", "-Wall"]
 
-SOURCES = ["engine.cu", "model.cu", "selftest.cu", "host_graph.cpp", "host_params.cpp"]
-HEADERS = ["common.hpp", "engine_ctx.hpp", "mlp_generic.cuh", "model_kernels.cuh", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh"]
+SOURCES = ["engine.cu", "model.cu", "host_graph.cpp", "host_params.cpp"]
+DEBUG_SOURCES = ["selftest.cu"]
+HEADERS = ["common.hpp", "engine_ctx.hpp", "local_group.hpp", "mlp_generic.cuh", "model_kernels.cuh", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh"]
 
 
 def _newer(src: list[Path], out: Path) -> bool:
@@ -75,6 +77,18 @@ def build_library(verbose: bool = False, force: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    # debug aids live outside the product ABI, in their own library on top of it
+    dobjs = []
+    for s in DEBUG_SOURCES:
+        obj = OBJ_DIR / (s + ".o")
+        _compile(CSRC / s, obj, deps, verbose)
+        dobjs.append(obj)
+    if _newer(dobjs + [LIB], DEBUG_LIB) or force:
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(DEBUG_LIB), *map(str, dobjs), "-L", str(LIB_DIR), "-lhgnn_b200",
+               "-Xlinker", "-rpath,$ORIGIN", "-lcudart_static", "-lpthread", "-ldl", "-lrt"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"debug library link failed:\n{res.stdout}\n{res.stderr}")
     return LIB
 
 

@@ -34,6 +34,22 @@ void bind(hgnn_ctx* c) {
 }
 
 
+void allreduce_sum_f64(hgnn_ctx* c, double* d, int64_t n) {
+  if (c->nranks <= 1 || n <= 0) return;
+  if (c->comm) {
+    NCCL_OK(ncclAllReduce(d, d, (size_t)n, ncclDouble, ncclSum, c->comm, c->stream));
+  } else if (c->group) {
+    std::vector<double> h((size_t)n);
+    CUDA_OK(cudaMemcpyAsync(h.data(), d, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->group->allreduce_sum(c->rank, h);
+    CUDA_OK(cudaMemcpyAsync(d, h.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+  } else {
+    fail(HGNN_ERR_CONFIG, "all_reduce_sum: no rank runtime");
+  }
+}
+
 void check_launch(hgnn_ctx* c) {
   c->launches += 1;
   CUDA_OK(cudaGetLastError());
@@ -247,8 +263,134 @@ void edges_to_host(hgnn_ctx* c, const float* d, double* h) {
 // --------------------------------------------------------------------------
 // halo exchange (comm.cpp:281-357) over NCCL point-to-point
 // --------------------------------------------------------------------------
+// ---- in-process rank group (LocalGroup): the same exchange, with the NCCL
+// transfers replaced by device-to-device copies between the ranks' buffers.
+// Phase 1: every rank exposes a buffer (event ev_pub) and meets its peers;
+// each then pulls what the peers expose for it; phase 2: every rank records
+// ev_consumed after its pulls, meets its peers again, and orders its stream
+// after the peers' pulls before it may overwrite the exposed buffer.
+int nbr_index(const hgnn_ctx* p, int32_t r) {
+  for (size_t n = 0; n < p->h_nbr.size(); ++n)
+    if (p->h_nbr[n] == r) return (int)n;
+  return -1;
+}
+
+template <class Pull>
+void local_exchange(hgnn_ctx* c, int kind, const float* exposed, cudaStream_t st, Pull&& pull) {
+  LocalGroup& G = *c->group;
+  c->xpub = exposed;
+  CUDA_OK(cudaEventRecord(c->ev_pub, st));
+  const CollSig sig{kind, c->mode, c->H};
+  G.barrier(c->rank, sig);
+  try {
+    pull(G);
+    CUDA_OK(cudaEventRecord(c->ev_consumed, st));
+  } catch (const Error& e) {
+    G.abort(std::string("rank ") + std::to_string(c->rank) + ": " + e.what());
+    throw;
+  }
+  G.barrier(c->rank, CollSig{kCollDone, c->mode, c->H});
+  for (int32_t r = 0; r < G.R; ++r)
+    if (r != c->rank) CUDA_OK(cudaStreamWaitEvent(st, G.ctx[(size_t)r]->ev_consumed, 0));
+}
+
+void copy_from_peer(hgnn_ctx* c, float* dst, const hgnn_ctx* p, const float* src, int64_t n_floats,
+                    cudaStream_t st) {
+  if (n_floats <= 0) return;
+  CUDA_OK(cudaStreamWaitEvent(st, p->ev_pub, 0));
+  CUDA_OK(cudaMemcpyPeerAsync(dst, c->device, src, p->device, sizeof(float) * (size_t)n_floats, st));
+}
+
+void local_halo_exchange(hgnn_ctx* c, float* a, cudaStream_t st) {
+  const int64_t H = c->H;
+  const int R = c->nranks;
+  if (c->mode == HGNN_MODE_NA2A) {
+    if (c->n_send > 0) {
+      gather_rows_kernel<<<blocks_for(c->n_send * H / 4), kEwThreads, 0, st>>>(a, c->send_rows.p, nullptr,
+                                                                                     c->n_send, (int)H, c->sendbuf.p);
+      check_launch(c);
+    }
+    local_exchange(c, kCollHaloFwd, c->sendbuf.p, st, [&](LocalGroup& G) {
+      for (size_t n = 0; n < c->h_nbr.size(); ++n) {  // pull neighbour n's send block for this rank
+        const hgnn_ctx* p = G.ctx[(size_t)c->h_nbr[n]];
+        const int j = nbr_index(p, c->rank);
+        const int64_t cr = c->h_recv_off[n + 1] - c->h_recv_off[n];
+        if (j < 0 || p->h_send_off[(size_t)j + 1] - p->h_send_off[(size_t)j] != cr)
+          fail(HGNN_ERR_COLLECTIVE, "halo_exchange: send / receive masks of ranks " + std::to_string(p->rank) +
+                                        " and " + std::to_string(c->rank) + " do not pair");
+        copy_from_peer(c, a + c->h_recv_base[n] * H, p, p->xpub + (int64_t)p->h_send_off[(size_t)j] * H, cr * H, st);
+        c->halo_bytes += cr * H * (int64_t)sizeof(float);
+      }
+    });
+  } else if (c->mode == HGNN_MODE_A2A) {
+    const int64_t pad = c->max_buffer_rows;
+    if (pad == 0 || R == 1) return;
+    CUDA_OK(cudaMemsetAsync(c->sendbuf.p, 0, sizeof(float) * (size_t)(R * pad * H), st));
+    if (c->n_send > 0) {
+      gather_rows_kernel<<<blocks_for(c->n_send * H / 4), kEwThreads, 0, st>>>(
+          a, c->send_rows.p, c->pos_a2a_send.p, c->n_send, (int)H, c->sendbuf.p);
+      check_launch(c);
+    }
+    local_exchange(c, kCollHaloFwd, c->sendbuf.p, st, [&](LocalGroup& G) {
+      for (int d = 0; d < R; ++d) {  // padded block of every rank (itself included), comm.cpp:297-298
+        const hgnn_ctx* p = G.ctx[(size_t)d];
+        if (p->max_buffer_rows != pad) fail(HGNN_ERR_COLLECTIVE, "all_to_all (A2A): buffers must be padded to one common size");
+        copy_from_peer(c, c->recvbuf.p + (int64_t)d * pad * H, p, p->xpub + (int64_t)c->rank * pad * H, pad * H, st);
+      }
+      c->halo_bytes += (int64_t)R * pad * H * (int64_t)sizeof(float);
+    });
+    if (c->n_recv > 0) {
+      scatter_rows_kernel<<<blocks_for(c->n_recv * H / 4), kEwThreads, 0, st>>>(
+          c->recvbuf.p, c->pos_a2a_recv.p, c->recv_rows.p, c->n_recv, (int)H, a);
+      check_launch(c);
+    }
+  }
+}
+
+// Adjoint (comm.cpp:317-357): rank c pulls, for each neighbour p, p's halo
+// adjoint block of the rows c sent it into recvbuf at c's send offsets.
+void local_halo_exchange_adjoint(hgnn_ctx* c, float* d_a, cudaStream_t st) {
+  const int64_t H = c->H;
+  const int R = c->nranks;
+  if (c->mode == HGNN_MODE_NA2A) {
+    local_exchange(c, kCollHaloAdj, d_a, st, [&](LocalGroup& G) {
+      for (size_t n = 0; n < c->h_nbr.size(); ++n) {
+        const hgnn_ctx* p = G.ctx[(size_t)c->h_nbr[n]];
+        const int j = nbr_index(p, c->rank);
+        const int64_t cs = c->h_send_off[n + 1] - c->h_send_off[n];
+        if (j < 0 || p->h_recv_off[(size_t)j + 1] - p->h_recv_off[(size_t)j] != cs)
+          fail(HGNN_ERR_COLLECTIVE, "halo_exchange_adjoint: masks of ranks " + std::to_string(p->rank) + " and " +
+                                        std::to_string(c->rank) + " do not pair");
+        copy_from_peer(c, c->recvbuf.p + (int64_t)c->h_send_off[n] * H, p, p->xpub + p->h_recv_base[(size_t)j] * H,
+                       cs * H, st);
+        c->halo_bytes += cs * H * (int64_t)sizeof(float);
+      }
+    });
+  } else if (c->mode == HGNN_MODE_A2A) {
+    const int64_t pad = c->max_buffer_rows;
+    if (pad == 0 || R == 1) return;
+    CUDA_OK(cudaMemsetAsync(c->sendbuf.p, 0, sizeof(float) * (size_t)(R * pad * H), st));
+    if (c->n_recv > 0) {
+      gather_rows_kernel<<<blocks_for(c->n_recv * H / 4), kEwThreads, 0, st>>>(
+          d_a, c->recv_rows.p, c->pos_a2a_recv.p, c->n_recv, (int)H, c->sendbuf.p);
+      check_launch(c);
+    }
+    local_exchange(c, kCollHaloAdj, c->sendbuf.p, st, [&](LocalGroup& G) {
+      for (int d = 0; d < R; ++d) {
+        const hgnn_ctx* p = G.ctx[(size_t)d];
+        copy_from_peer(c, c->recvbuf.p + (int64_t)d * pad * H, p, p->xpub + (int64_t)c->rank * pad * H, pad * H, st);
+      }
+      c->halo_bytes += (int64_t)R * pad * H * (int64_t)sizeof(float);
+    });
+  }
+}
+
 void halo_exchange(hgnn_ctx* c, float* a, cudaStream_t st) {
   Timed t(c, HGNN_K_HALO, st);
+  if (c->group) {
+    local_halo_exchange(c, a, st);
+    return;
+  }
   const int64_t H = c->H;
   const int R = c->nranks;
   if (c->mode == HGNN_MODE_NA2A) {
@@ -298,7 +440,11 @@ void halo_exchange_adjoint(hgnn_ctx* c, float* d_a, cudaStream_t st) {
   const int64_t H = c->H;
   const int R = c->nranks;
   const int64_t* acc_pos = nullptr;
-  if (c->mode == HGNN_MODE_NA2A) {
+  if (c->group) {
+    if (c->mode == HGNN_MODE_NONE || (c->mode == HGNN_MODE_A2A && (c->max_buffer_rows == 0 || R == 1))) return;
+    local_halo_exchange_adjoint(c, d_a, st);
+    acc_pos = c->mode == HGNN_MODE_NA2A ? c->acc_pos_na2a.p : c->acc_pos_a2a.p;
+  } else if (c->mode == HGNN_MODE_NA2A) {
     if (R > 1 && !c->h_nbr.empty()) {
       NCCL_OK(ncclGroupStart());
       for (size_t n = 0; n < c->h_nbr.size(); ++n) {
@@ -448,7 +594,8 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   float* e2 = c->es[m + 1]->p;
   float* a = c->as[m]->p;
   float* x2 = c->xs[m + 1]->p;
-  if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && c->comm && c->n_rows_bnd > 0 && use_tc(c)) {
+  if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group) && c->n_rows_bnd > 0 &&
+      use_tc(c)) {
     // Overlapped schedule, same results: boundary-row edges + aggregates,
     // then the exchange on the side stream while the interior edges run on
     // all but halo_sm_reserve SMs (left to the pack and NCCL kernels).
@@ -569,7 +716,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       if (c->nl > 0) reduce_grads(c, c->grid_node_b, c->n_node_par, c->grads.p + goff + c->n_edge_par);
     }
   }
-  if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && c->comm && c->n_rows_bnd > 0 &&
+  if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group) && c->n_rows_bnd > 0 &&
       use_tc_bwd(c)) {
     // Overlapped schedule: sync adjoint, then the adjoint exchange on the side
     // stream while the interior edges (receivers whose d_a the exchange does
@@ -697,7 +844,7 @@ void require_ready(hgnn_ctx* c) {
   if (!c->configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_configure has not been called");
   if (!c->graph_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_graph_upload has not been called");
   if (!c->params_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_params_upload has not been called");
-  if (c->mode != HGNN_MODE_NONE && c->nranks > 1 && !c->comm)
+  if (c->mode != HGNN_MODE_NONE && c->nranks > 1 && !c->comm && !c->group)
     fail(HGNN_ERR_CONFIG, "nmp_layer: exchange mode requires a rank runtime");
 }
 
@@ -720,6 +867,48 @@ int hgnn_nccl_unique_id(uint8_t out[128]) {
     ncclUniqueId id;
     NCCL_OK(ncclGetUniqueId(&id));
     std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int hgnn_local_group_create(int32_t num_ranks, hgnn_local_group** out) {
+  return guarded([&] {
+    if (!out) fail(HGNN_ERR_CONFIG, "hgnn_local_group_create: null output");
+    if (num_ranks < 1) fail(HGNN_ERR_CONFIG, "RankRuntime: need at least one rank");
+    *out = reinterpret_cast<hgnn_local_group*>(new LocalGroup(num_ranks));
+  });
+}
+
+int hgnn_local_group_destroy(hgnn_local_group* g) {
+  return guarded([&] { delete reinterpret_cast<LocalGroup*>(g); });
+}
+
+int hgnn_local_group_set_timeout(hgnn_local_group* g, int64_t timeout_ms) {
+  return guarded([&] {
+    if (!g || timeout_ms <= 0) fail(HGNN_ERR_CONFIG, "hgnn_local_group_set_timeout: bad arguments");
+    reinterpret_cast<LocalGroup*>(g)->timeout_ms = timeout_ms;
+  });
+}
+
+int hgnn_ctx_create_local(int device, int32_t rank, hgnn_local_group* group, hgnn_ctx** out) {
+  return guarded([&] {
+    if (!group) fail(HGNN_ERR_CONFIG, "hgnn_ctx_create_local: null group");
+    LocalGroup* G = reinterpret_cast<LocalGroup*>(group);
+    if (rank < 0 || rank >= G->R) fail(HGNN_ERR_CONFIG, "hgnn_ctx_create_local: bad rank");
+    hgnn_ctx* c = nullptr;
+    const int rc = hgnn_ctx_create(device, rank, 1, nullptr, &c);
+    if (rc != HGNN_OK) fail(rc, hgnn_last_error());
+    c->nranks = G->R;
+    c->group = G;
+    try {
+      CUDA_OK(cudaEventCreateWithFlags(&c->ev_pub, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&c->ev_consumed, cudaEventDisableTiming));
+      G->attach(rank, c);
+    } catch (...) {
+      c->group = nullptr;
+      hgnn_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
   });
 }
 
@@ -765,6 +954,9 @@ int hgnn_ctx_destroy(hgnn_ctx* c) {
         cudaEventDestroy(p.b);
       }
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->group) c->group->retire(c->rank);
+    if (c->ev_pub) cudaEventDestroy(c->ev_pub);
+    if (c->ev_consumed) cudaEventDestroy(c->ev_consumed);
     if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     if (c->side) cudaStreamDestroy(c->side);
@@ -852,6 +1044,8 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
     c->slot_of.upload(slot_of.data(), ne, c->stream);
     c->inv.upload(inv_s.data(), ne, c->stream);
     if (g->node_inv_degree) c->node_inv.upload(g->node_inv_degree, nl, c->stream);
+    else c->node_inv.release();
+    c->model_data_ready = false;  // features / targets were sized for the previous graph
     c->seg_beg.upload(seg_b.data(), rows, c->stream);
     c->seg_end.upload(seg_e.data(), rows, c->stream);
     c->ne_bnd = ne_bnd;
@@ -874,7 +1068,9 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
       if (g->neighbors[n] < 0 || g->neighbors[n] >= c->nranks || g->neighbors[n] == c->rank ||
           (n > 0 && g->neighbors[n] <= g->neighbors[n - 1]))
         fail(HGNN_ERR_INTEGRITY, "neighbors must be ascending peer ranks");
-      const int64_t base = g->recv_rows[c->h_recv_off[(size_t)n]];
+      // an empty receive block has no base row (and its first index may be nh)
+      const bool empty_recv = c->h_recv_off[(size_t)n + 1] == c->h_recv_off[(size_t)n];
+      const int64_t base = empty_recv ? nl : g->recv_rows[c->h_recv_off[(size_t)n]];
       c->h_recv_base[(size_t)n] = base;
       for (int32_t t = c->h_recv_off[(size_t)n]; t < c->h_recv_off[(size_t)n + 1]; ++t)
         if (g->recv_rows[t] != base + (t - c->h_recv_off[(size_t)n]))
@@ -919,7 +1115,22 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
     c->acc_off.upload(acc_off.data(), (int64_t)acc_off.size(), c->stream);
     c->acc_pos_na2a.upload(pos_n.data(), (int64_t)pos_n.size(), c->stream);
     c->acc_pos_a2a.upload(pos_a.data(), (int64_t)pos_a.size(), c->stream);
-    // sync groups
+    // sync groups: sync_kernel writes each group's local row in place and
+    // reads its slots, so a slot must be -1 (the row itself) or a halo row
+    // (never written by the sync), and each local row may own one group
+    {
+      std::vector<uint8_t> owned((size_t)nl, 0);
+      for (int64_t q = 0; q < g->num_sync_groups; ++q) {
+        const int32_t li = g->sync_local[q];
+        if (li < 0 || li >= nl || owned[(size_t)li]) fail(HGNN_ERR_INTEGRITY, "sync group local rows must be distinct local rows");
+        owned[(size_t)li] = 1;
+        if (g->sync_offsets[q + 1] < g->sync_offsets[q]) fail(HGNN_ERR_INTEGRITY, "sync offsets must be ascending");
+        for (int32_t t = g->sync_offsets[q]; t < g->sync_offsets[q + 1]; ++t) {
+          const int32_t sl = g->sync_slots[t];
+          if (sl != -1 && (sl < nl || sl >= rows)) fail(HGNN_ERR_INTEGRITY, "sync slots must be -1 or halo rows");
+        }
+      }
+    }
     c->n_sync = g->num_sync_groups;
     c->sync_local.upload(g->sync_local, c->n_sync, c->stream);
     c->sync_off.upload(g->sync_offsets, c->n_sync + 1, c->stream);
@@ -941,10 +1152,13 @@ int hgnn_configure(hgnn_ctx* c, int64_t hidden, int64_t M, int64_t k, int mode) 
     if (M < 0) fail(HGNN_ERR_CONFIG, "GnnConfig: num_mp_layers must be >= 0");
     if (k < 0 || k > 16) fail(HGNN_ERR_CONFIG, "GnnConfig: mlp_hidden_layers must be in [0, 16]");
     if (mode < HGNN_MODE_NONE || mode > HGNN_MODE_NA2A) fail(HGNN_ERR_CONFIG, "unknown exchange mode");
-    if (mode != HGNN_MODE_NONE && c->nranks > 1 && !c->comm)
+    if (mode != HGNN_MODE_NONE && c->nranks > 1 && !c->comm && !c->group)
       fail(HGNN_ERR_CONFIG, "nmp_layer: exchange mode requires a rank runtime");
     if (c->H != hidden || c->M != M || c->K != k) {
+      // every size derived from (H, M, k) is stale: the MP parameters and the
+      // model level's layout (off_mp, n_full, ...) must be set up again
       c->params_ready = false;
+      c->model_configured = c->model_params_ready = c->model_data_ready = false;
       c->xs.clear();
       c->es.clear();
       c->as.clear();

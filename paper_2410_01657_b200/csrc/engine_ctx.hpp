@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "local_group.hpp"
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
 
@@ -66,6 +67,11 @@ struct hgnn_ctx {
   int32_t rank = 0, nranks = 1;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  // in-process rank group (hgnn_ctx_create_local): the exchange and the
+  // all-reduces rendezvous on the host and copy device-to-device
+  hgnn_b200::LocalGroup* group = nullptr;
+  cudaEvent_t ev_pub = nullptr, ev_consumed = nullptr;  // exposed buffer ready / peers' reads done
+  const float* xpub = nullptr;                          // buffer this rank exposes to its peers
   int num_sms = 148;
 
   // configuration
@@ -225,6 +231,9 @@ inline int64_t chunk_floats_fwd(int in_dim, int H, int K) { return (int64_t)(in_
 inline int64_t chunk_floats_bwd(int in_dim, int H, int K) { return (int64_t)(2 * (in_dim / H) + 2 * K + 1) * 2 * H * H; }
 
 void bind(hgnn_ctx* c);
+// in-place sum over ranks of n device doubles on the compute stream (NCCL, or
+// the in-process group's host rendezvous in rank order)
+void allreduce_sum_f64(hgnn_ctx* c, double* d, int64_t n);
 void check_launch(hgnn_ctx* c);
 bool tc_eligible(const hgnn_ctx* c);
 void ensure_buffers(hgnn_ctx* c);

@@ -601,7 +601,8 @@ std::unique_ptr<HostGraph> load_binary(const std::string& path) {
   check_index(hg->send_rows, 0, nl, path + ": send mask");
   check_index(hg->recv_rows, nl, rows, path + ": recv mask");
   check_index(hg->sync_local, 0, nl, path + ": sync group");
-  check_index(hg->sync_slots, -1, rows, path + ": sync slot");
+  for (int32_t x : hg->sync_slots)  // -1 = the local row itself, else a halo row (graph.cpp:203-228)
+    if (x != -1 && (x < nl || x >= rows)) fail(HGNN_ERR_IO, path + ": sync slot index out of range");
   for (int32_t d : hg->node_degree)
     if (d < 1) fail(HGNN_ERR_IO, path + ": node_degree must be >= 1");
   for (int32_t d : hg->edge_degree)

@@ -103,7 +103,7 @@ void model_compute_gradients(hgnn_ctx* c) {
   check_launch(c);
   loss_final_kernel<<<1, 32, 0, c->stream>>>(c->loss_part.p, kLossBlocks, c->loss_st.p);
   check_launch(c);
-  if (c->nranks > 1) NCCL_OK(ncclAllReduce(c->loss_st.p, c->loss_st.p, 2, ncclDouble, ncclSum, c->comm, c->stream));
+  if (c->nranks > 1) allreduce_sum_f64(c, c->loss_st.p, 2);
   loss_seed_kernel<<<1, 32, 0, c->stream>>>(c->loss_st.p, (int)c->fy, c->nranks);
   check_launch(c);
   loss_backward_kernel<<<blocks_for(nl * c->fy), kEwThreads, 0, c->stream>>>(
@@ -127,7 +127,7 @@ void model_compute_gradients(hgnn_ctx* c) {
   }
   // average over ranks (model.cpp:516-531)
   if (c->nranks > 1) {
-    NCCL_OK(ncclAllReduce(c->mgrads.p, c->mgrads.p, (size_t)c->n_full, ncclDouble, ncclSum, c->comm, c->stream));
+    allreduce_sum_f64(c, c->mgrads.p, c->n_full);
     scale_f64_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mgrads.p, c->n_full,
                                                                            1.0 / (double)c->nranks);
     check_launch(c);
@@ -306,19 +306,24 @@ int hgnn_train_step(hgnn_ctx* c, double lr, double beta1, double beta2, double e
     bind(c);
     require_model(c);
     model_compute_gradients(c);
-    c->adam_step += 1;
-    const double bc1 = 1.0 - std::pow(beta1, (double)c->adam_step);
-    const double bc2 = 1.0 - std::pow(beta2, (double)c->adam_step);
     Timed t(c, HGNN_K_LOSS_ADAM);
     CUDA_OK(cudaMemsetAsync(c->nonfinite.p, 0, sizeof(int), c->stream));
-    adam_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->mgrads.p, c->adam_m.p,
-                                                                     c->adam_v.p, c->n_full, lr, beta1, beta2, eps,
-                                                                     bc1, bc2, c->nonfinite.p);
+    nonfinite_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mgrads.p, c->n_full, c->nonfinite.p);
     check_launch(c);
     int bad = 0;
     CUDA_OK(cudaMemcpyAsync(&bad, c->nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
+    // same error as nn.cpp:352; unlike the reference (which has updated the
+    // elements before the bad one) no state changes, so the fp64 master and
+    // its fp32 / tf32 working copies stay consistent
     if (bad) fail(HGNN_ERR_OPTIMIZER, "adam_step: non-finite gradient");
+    c->adam_step += 1;
+    const double bc1 = 1.0 - std::pow(beta1, (double)c->adam_step);
+    const double bc2 = 1.0 - std::pow(beta2, (double)c->adam_step);
+    adam_kernel<<<blocks_for(c->n_full), kEwThreads, 0, c->stream>>>(c->mparams.p, c->mgrads.p, c->adam_m.p,
+                                                                     c->adam_v.p, c->n_full, lr, beta1, beta2, eps,
+                                                                     bc1, bc2);
+    check_launch(c);
     model_refresh_params(c);
     t.stop();
     CUDA_OK(cudaStreamSynchronize(c->stream));

@@ -89,16 +89,20 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int64_t b
 
 // Bias-corrected Adam (nn.cpp:331-360), fp64 master parameters; flags any
 // non-finite gradient (OptimizerError in the reference).
+// Pass 1 of adam_step (nn.cpp:331-360): flag any non-finite gradient. The
+// reference throws before touching a parameter, so the update runs only when
+// this pass found none (all state stays consistent on failure).
+__global__ void nonfinite_kernel(const double* __restrict__ g, int64_t n, int* __restrict__ nonfinite) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(g[i])) atomicExch(nonfinite, 1);
+}
+
 __global__ void adam_kernel(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
                             double* __restrict__ v, int64_t n, double lr, double b1, double b2, double eps,
-                            double bc1, double bc2, int* __restrict__ nonfinite) {
+                            double bc1, double bc2) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double gi = g[i];
-  if (!isfinite(gi)) {
-    atomicExch(nonfinite, 1);
-    return;
-  }
   const double mi = b1 * m[i] + (1.0 - b1) * gi;
   const double vi = b2 * v[i] + (1.0 - b2) * gi * gi;
   m[i] = mi;

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <vector>
 
+#include "../../include/hgnn_b200_debug.h"
 #include "common.hpp"
 #include "tc_ptx.cuh"
 

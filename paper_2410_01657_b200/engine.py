@@ -40,11 +40,60 @@ def _out(a: np.ndarray, shape) -> np.ndarray:
     return a.reshape(shape)
 
 
-class Engine:
-    def __init__(self, device: int = 0, rank: int = 0, num_ranks: int = 1, uid: bytes | None = None):
+class LocalGroup:
+    """In-process rank group (the reference's RankRuntime, comm.cpp:35-93): R
+    Engines, one per rank, driven by R host threads of this process (one GPU or
+    several). Every collective rendezvous checks that all ranks post the same
+    collective in the same order (CollectiveError otherwise, comm.cpp:168-208)
+    and times out instead of hanging."""
+
+    def __init__(self, num_ranks: int, timeout_ms: int | None = None):
         self._h = C.c_void_p()
-        uid_buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
-        N.check(N.LIB.hgnn_ctx_create(device, rank, num_ranks, uid_buf, C.byref(self._h)))
+        N.check(N.LIB.hgnn_local_group_create(num_ranks, C.byref(self._h)))
+        self.num_ranks = num_ranks
+        if timeout_ms is not None:
+            N.check(N.LIB.hgnn_local_group_set_timeout(self._h, int(timeout_ms)))
+
+    def engine(self, rank: int, device: int = 0) -> "Engine":
+        return Engine(device, rank, self.num_ranks, group=self)
+
+    def run(self, body, engines):
+        """Runs body(engine) on one thread per rank (RankRuntime::run); returns
+        the per-rank results and re-raises the first failure after all joined."""
+        import threading
+        out, err = [None] * len(engines), [None] * len(engines)
+
+        def work(r):
+            try:
+                out[r] = body(engines[r])
+            except BaseException as e:  # noqa: BLE001
+                err[r] = e
+        ts = [threading.Thread(target=work, args=(r,)) for r in range(len(engines))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+
+    def close(self) -> None:
+        if self._h:
+            N.check(N.LIB.hgnn_local_group_destroy(self._h))
+            self._h = C.c_void_p()
+
+
+class Engine:
+    def __init__(self, device: int = 0, rank: int = 0, num_ranks: int = 1, uid: bytes | None = None,
+                 group: LocalGroup | None = None):
+        self._h = C.c_void_p()
+        if group is not None:
+            N.check(N.LIB.hgnn_ctx_create_local(device, rank, group._h, C.byref(self._h)))
+            num_ranks = group.num_ranks
+        else:
+            uid_buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
+            N.check(N.LIB.hgnn_ctx_create(device, rank, num_ranks, uid_buf, C.byref(self._h)))
         self.rank, self.num_ranks, self.device = rank, num_ranks, device
         self.graph: RankGraph | None = None
         self.cfg: GnnConfig | None = None

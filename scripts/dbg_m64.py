@@ -7,7 +7,7 @@ B = rng.integers(-3, 4, (32, 128)).astype(np.float32)
 ref = A[:64].astype(np.float64) @ B[:, :64].astype(np.float64)  # 64 x 64
 for mode in (9, 10):
     D = np.zeros((128, 128), np.float32)
-    st = N.LIB.hgnn_selftest_mma(mode, A.ctypes.data, B.ctypes.data, D.ctypes.data)
+    st = N.debug_lib().hgnn_selftest_mma(mode, A.ctypes.data, B.ctypes.data, D.ctypes.data)
     print("mode", mode, "status", st, "nonzero lanes", np.nonzero(np.abs(D).sum(1))[0][[0, -1]] if np.count_nonzero(D) else None,
           "nonzero cols", np.nonzero(np.abs(D).sum(0))[0][[0, -1]] if np.count_nonzero(D) else None)
     # locate each reference row

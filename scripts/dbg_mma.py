@@ -7,7 +7,7 @@ B = rng.integers(-3, 4, (32, 128)).astype(np.float32)
 ref = A.astype(np.float64) @ B.astype(np.float64)
 for mode in (0, 2, 6, 7, 8):
     D = np.zeros((128, 128), np.float32)
-    st = N.LIB.hgnn_selftest_mma(mode, A.ctypes.data, B.ctypes.data, D.ctypes.data)
+    st = N.debug_lib().hgnn_selftest_mma(mode, A.ctypes.data, B.ctypes.data, D.ctypes.data)
     err = np.abs(D - ref).max()
     print("mode", mode, "status", st, "max err", err, "nonzero", np.count_nonzero(D), "D[0,:4]", D[0,:4], "ref", ref[0,:4])
     if err > 0:

@@ -26,6 +26,7 @@ GRAPH_CASES = [  # (E, p, R, strategy, factors)
     (2, 2, 1, "verify", None), (2, 2, 4, "verify", None), (2, 1, 2, "slab", None), (2, 5, 2, "slab", None),
     (4, 2, 8, "verify", None), (4, 3, 8, "verify", None), (6, 2, 6, "block", None), (4, 2, 8, "block", (2, 2, 2)),
     (3, 2, 3, "slab", None), (4, 3, 2, "block", (1, 2, 1)),
+    (16, 3, 1, "verify", None), (16, 3, 2, "verify", None),  # BASELINE configs[0] (C1) and configs[1] (C2)
 ]
 GRAPH_FIELDS = ["global_ids", "positions", "edge_src", "edge_dst", "node_degree", "edge_degree", "node_inv_degree",
                 "edge_inv_degree", "in_offsets", "in_edges", "out_offsets", "out_edges", "neighbors", "send_offsets",
@@ -92,6 +93,8 @@ def main() -> None:
                "c1_large_loss_seed0": 1670973.5417324416},
               open(OUT / "reference_hashes.json", "w"), indent=1, sort_keys=True)
 
+    if "--hashes-only" in sys.argv:
+        return
     for name, E, p, R, H, M, k, mode, seed in MP_CASES:
         ref = O.RefGraph(E, p, R, "verify", features=False)
         n_mp = O.ref_lib().ref_mp_param_count(H, M, k)

@@ -1,0 +1,86 @@
+"""GPU parity at BASELINE.json's own configurations, against the reference
+itself (oracle/_ref: /root/reference/proj compiled in place, fp64, OpenMP).
+
+  * configs[0] (C1) at full size: 16^3 elements, P=3 (117,649 nodes, 691,488
+    directed edges), H32, k5, M4 — the MP stack of the `large` preset, forward
+    (every layer's a_sync, x_out, e_out) and backward (dx0, de0, every
+    gradient tensor);
+  * the configs[2] model shape (H64, k5, M4) on a 6^3-element P=5 box, the
+    largest P=5 mesh the reference finishes in seconds: error growth through
+    all four layers of the bench's layer stack.
+
+Tolerances as tests/test_gpu_parity.py: per tensor, normalised by the
+tensor's max |ref| (fixtures.hpp:56-70, harness.cpp:201-212): FWD_TOL for
+layer outputs / aggregates, BWD_TOL for adjoints and gradients.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2410_01657_b200 import Engine, GnnConfig, build_rank_graph, init_params, mp_layer_slices, mp_params
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+from rank_worker import gid_inputs  # noqa: E402
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not O.ref_available(), reason="needs the reference compiled in place (oracle/_ref)")]
+FWD_TOL = 5e-5
+BWD_TOL = 2e-4
+
+
+def rel(test, ref):
+    mag = np.abs(ref).max()
+    return float(np.abs(test - ref).max() / (mag if mag > 0 else 1.0))
+
+
+@pytest.fixture(scope="module")
+def engine(gpus):
+    eng = Engine(0)
+    yield eng
+    eng.close()
+
+
+def check_against_reference(engine, E, p, H, M, k, seed):
+    cfg = GnnConfig("cfg", H, M, k, mode="na2a")
+    mp = mp_params(cfg, init_params(cfg, seed))
+    g = build_rank_graph(E, p, 1, 0, "verify")
+    x0, e0, dx = gid_inputs(g, H)
+    engine.upload_graph(g)
+    engine.configure(cfg)
+    engine.upload_params(mp)
+    engine.nmp_forward(x0, e0)
+    tr = {m: {w: engine.trace(m, w) for w in ("a_sync", "x_out", "e_out")} for m in range(M)}
+    dx0, de0, grads = engine.nmp_backward(dx)
+    ref = O.ref_mp_run(O.RefGraph(E, p, 1, "verify", features=False), H, M, k, "na2a", mp, [x0], [e0], [dx])
+    worst = {}
+    for m in range(M):
+        for w in ("a_sync", "x_out", "e_out"):
+            worst[f"{w}{m}"] = rel(tr[m][w], ref.get(0, w, m))
+    worst["dx0"] = rel(dx0, ref.get(0, "dx_in", 0))
+    worst["de0"] = rel(de0, ref.get(0, "de_in", 0))
+    rg = ref.get(0, "mp_grads")
+    for name, a, b in mp_layer_slices(cfg):
+        worst[name] = rel(grads[a:b], rg[a:b])
+    fwd = {n: v for n, v in worst.items() if n[:1] in "axe" and not n.startswith("layer")}
+    bwd = {n: v for n, v in worst.items() if n not in fwd}
+    print(f"\nE={E} p={p} H={H} M={M} k={k}: worst fwd {max(fwd.values()):.2e} ({max(fwd, key=fwd.get)}), "
+          f"worst bwd {max(bwd.values()):.2e} ({max(bwd, key=bwd.get)})")
+    for n, v in fwd.items():
+        assert v < FWD_TOL, (n, v)
+    for n, v in bwd.items():
+        assert v < BWD_TOL, (n, v)
+
+
+def test_c1_full_size_mp_stack(engine):
+    """configs[0]: 16^3 / P=3, H32, k5, M4, against the reference's MP stack."""
+    check_against_reference(engine, 16, 3, 32, 4, 5, seed=0)
+
+
+def test_bench_shape_h64_k5_m4(engine):
+    """configs[2]'s layer stack (H64, k5, M4) on a 6^3 / P=5 box."""
+    check_against_reference(engine, 6, 5, 64, 4, 5, seed=0)

@@ -1,0 +1,226 @@
+"""Multi-rank consistency on ONE GPU: R ranks as host threads of one process
+(LocalGroup = the reference's RankRuntime, comm.cpp:35-93), each with its own
+device context, exchanging through device-to-device copies. This runs the
+halo path of the device engine — pack (gather_rows), the exchange semantics of
+comm.cpp:281-357 in both modes, the ascending-owner sync (model.cpp:243-257),
+the sync / exchange adjoints and the adjoint accumulation (model.cpp:343-351,
+comm.cpp:344-356) — on a single B200:
+
+  * each rank matches the reference's own R-rank run (golden fixtures from
+    oracle/_ref) and the R-rank oracle;
+  * C2 (BASELINE configs[1]: 16^3/P3 split 2-way, H32 k5 M4): the 2-rank
+    output equals the 1-rank output by global id, coincident copies are
+    bitwise equal, summed rank gradients equal the 1-rank gradients
+    (test_model.cpp:145-183, harness.cpp:147-158 / 201-212);
+  * the overlapped and serial schedules agree;
+  * a mismatched collective sequence raises CollectiveError on every rank
+    (comm.cpp:184-188) and a missing rank times out instead of hanging.
+
+Tolerances as tests/test_gpu_parity.py (fp32 device vs fp64 reference, per
+tensor normalised by max |ref|): FWD_TOL outputs, BWD_TOL adjoints / gradients.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2410_01657_b200 import (CollectiveError, GnnConfig, LocalGroup, build_distributed_graph, init_params,
+                                   mp_layer_slices, mp_params)
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+from rank_worker import gid_inputs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+FWD_TOL = 5e-5
+BWD_TOL = 2e-4
+MODES = {0: "none", 1: "a2a", 2: "na2a"}
+
+
+def rel(test, ref):
+    mag = np.abs(ref).max()
+    return float(np.abs(test - ref).max() / (mag if mag > 0 else 1.0))
+
+
+def run_group(graphs, cfg, mp, inputs, *, options=None, traces=False):
+    """One MP-stack forward + backward on len(graphs) ranks of one GPU."""
+    R = len(graphs)
+    grp = LocalGroup(R, timeout_ms=60000)
+    engines = [grp.engine(r) for r in range(R)]
+    try:
+        def body(eng):
+            r = eng.rank
+            eng.upload_graph(graphs[r])
+            eng.configure(cfg)
+            eng.upload_params(mp)
+            for k, v in (options or {}).items():
+                eng.set_option(k, v)
+            x0, e0, dx, de = inputs[r]
+            x_out, e_out = eng.nmp_forward(x0, e0, want_e=True)
+            tr = {m: eng.trace(m, "a_sync") for m in range(cfg.num_mp_layers)} if traces else None
+            dx0, de0, grads = eng.nmp_backward(dx, de)
+            return {"x_out": x_out, "e_out": e_out, "a_sync": tr, "dx0": dx0, "de0": de0, "grads": grads,
+                    "halo_bytes": eng.halo_bytes()}
+        return grp.run(body, engines)
+    finally:
+        for e in engines:
+            e.close()
+        grp.close()
+
+
+def by_gid(graphs, ys):
+    m, bitwise = {}, True
+    for g, y in zip(graphs, ys):
+        for i in range(g.num_local):
+            k = int(g.global_ids[i])
+            if k in m and m[k].tobytes() != y[i].tobytes():
+                bitwise = False
+            m.setdefault(k, y[i])
+    return m, bitwise
+
+
+@pytest.mark.parametrize("name", ["mp_e2p2_r4_h8", "mp_e2p2_r4_h8_a2a", "mp_e2p3_r2_h32"])
+def test_group_matches_reference_golden(gpus, golden_dir, name):
+    """The reference's own multi-rank run (fixtures from oracle/_ref, both exchange modes)."""
+    z = np.load(golden_dir / f"{name}.npz")
+    E, p, R, H, M, k, mode, seed = [int(v) for v in z["meta"]]
+    cfg = GnnConfig("g", H, M, k, mode=MODES[mode])
+    graphs = build_distributed_graph(E, p, R, "verify")
+    ins = [(z[f"r{r}_x0"], z[f"r{r}_e0"], z[f"r{r}_dx"], z[f"r{r}_de"]) for r in range(R)]
+    res = run_group(graphs, cfg, z["mp_params"], ins, traces=True)
+    for r in range(R):
+        assert rel(res[r]["x_out"], z[f"r{r}_x_out"]) < FWD_TOL, r
+        assert rel(res[r]["e_out"], z[f"r{r}_e_out"]) < FWD_TOL, r
+        assert rel(res[r]["a_sync"][0], z[f"r{r}_a_sync0"]) < FWD_TOL, r
+        assert rel(res[r]["dx0"], z[f"r{r}_dx0"]) < BWD_TOL, r
+        assert rel(res[r]["de0"], z[f"r{r}_de0"]) < BWD_TOL, r
+        for _, a, b in mp_layer_slices(cfg):
+            assert rel(res[r]["grads"][a:b], z[f"r{r}_grads"][a:b]) < BWD_TOL, r
+
+
+@pytest.mark.parametrize("R,E,p,H,M,k,mode", [(2, 3, 3, 64, 2, 5, "na2a"), (4, 4, 2, 64, 2, 2, "a2a"),
+                                              (8, 4, 2, 32, 2, 3, "na2a"), (8, 4, 2, 32, 1, 1, "a2a"),
+                                              (4, 4, 3, 16, 2, 2, "none")])
+def test_group_matches_oracle_and_is_consistent(gpus, R, E, p, H, M, k, mode):
+    cfg = GnnConfig("m", H, M, k, mode=mode)
+    mp = mp_params(cfg, init_params(cfg, 0))
+    graphs = build_distributed_graph(E, p, R, "verify")
+    ins = [gid_inputs(g, H) + (None,) for g in graphs]
+    res = run_group(graphs, cfg, mp, ins, traces=True)
+    ref = O.oracle_mp_run(graphs, H, M, k, mode, mp, [i[0] for i in ins], [i[1] for i in ins], [i[2] for i in ins])
+    for r in range(R):
+        for m in range(M):
+            assert rel(res[r]["a_sync"][m], ref["a_sync"][r][m]) < FWD_TOL, (r, m)
+        assert rel(res[r]["x_out"], ref["x_out"][r][M - 1]) < FWD_TOL, r
+        assert rel(res[r]["e_out"], ref["e_out"][r][M - 1]) < FWD_TOL, r
+        assert rel(res[r]["dx0"], ref["dx_in"][r][0]) < BWD_TOL, r
+        assert rel(res[r]["de0"], ref["de_in"][r][0]) < BWD_TOL, r
+        for _, a, b in mp_layer_slices(cfg):
+            assert rel(res[r]["grads"][a:b], ref["grads"][r][a:b]) < BWD_TOL, r
+    if mode == "none":
+        return
+    assert all(res[r]["halo_bytes"] > 0 for r in range(R))
+    mp_map, bitwise = by_gid(graphs, [res[r]["x_out"] for r in range(R)])
+    assert bitwise  # coincident copies bitwise equal (harness.cpp:147-158)
+    g1 = build_distributed_graph(E, p, 1, "verify")
+    i1 = gid_inputs(g1[0], H)
+    ref1 = O.oracle_mp_run(g1, H, M, k, mode, mp, [i1[0]], [i1[1]], [i1[2]])
+    one, _ = by_gid(g1, [ref1["x_out"][0][M - 1]])
+    mag = max(np.abs(v).max() for v in one.values())
+    assert max(np.abs(mp_map[gd] - one[gd]).max() for gd in one) / mag < FWD_TOL
+    gsum = sum(res[r]["grads"] for r in range(R))
+    for _, a, b in mp_layer_slices(cfg):
+        assert rel(gsum[a:b], ref1["grads"][0][a:b]) < BWD_TOL
+
+
+def test_c2_two_rank_consistency_full_size(gpus):
+    """BASELINE configs[1]: the configs[0] mesh (16^3 elements, P=3, 117,649
+    nodes) split 2-way, H32 k5 M4 (the `large` preset's MP stack): the 2-rank
+    device run equals the 1-rank device run by global id within FWD_TOL, the
+    coincident copies are bitwise equal across ranks, and the summed rank
+    gradients equal the 1-rank gradients within BWD_TOL (test_model.cpp:145-183)."""
+    E, p, H, M, k = 16, 3, 32, 4, 5
+    cfg = GnnConfig("c2", H, M, k, mode="na2a")
+    mp = mp_params(cfg, init_params(cfg, 0))
+    g2 = build_distributed_graph(E, p, 2, "verify")
+    g1 = build_distributed_graph(E, p, 1, "verify")
+    r2 = run_group(g2, cfg, mp, [gid_inputs(g, H) + (None,) for g in g2])
+    r1 = run_group(g1, cfg, mp, [gid_inputs(g1[0], H) + (None,)])
+    two, bitwise = by_gid(g2, [r["x_out"] for r in r2])
+    assert bitwise
+    one, _ = by_gid(g1, [r1[0]["x_out"]])
+    assert set(two) == set(one)
+    mag = max(np.abs(v).max() for v in one.values())
+    assert max(np.abs(two[gd] - one[gd]).max() for gd in one) / mag < FWD_TOL
+    gsum = r2[0]["grads"] + r2[1]["grads"]
+    for name, a, b in mp_layer_slices(cfg):
+        assert rel(gsum[a:b], r1[0]["grads"][a:b]) < BWD_TOL, name
+
+
+def test_overlapped_schedule_equals_serial_in_group(gpus):
+    """Outputs and input adjoints of the overlapped schedule are bitwise those
+    of the serial one; weight gradients only regroup fp32 partials."""
+    R, E, p, H, M, k = 2, 4, 3, 64, 2, 2
+    cfg = GnnConfig("o", H, M, k, mode="na2a")
+    mp = mp_params(cfg, init_params(cfg, 1))
+    graphs = build_distributed_graph(E, p, R, "verify")
+    ins = [gid_inputs(g, H) + (None,) for g in graphs]
+    a = run_group(graphs, cfg, mp, ins, options={"halo_overlap": 1})
+    b = run_group(graphs, cfg, mp, ins, options={"halo_overlap": 0})
+    for r in range(R):
+        for key in ("x_out", "e_out", "dx0", "de0"):
+            assert a[r][key].tobytes() == b[r][key].tobytes(), (r, key)
+        assert rel(a[r]["grads"], b[r]["grads"]) < 1e-5
+
+
+def test_mismatched_collective_sequence_raises(gpus):
+    """comm.cpp:184-188: ranks posting different collectives poison the group;
+    every rank gets CollectiveError (here: different exchange modes)."""
+    E, p, H = 2, 2, 8
+    graphs = build_distributed_graph(E, p, 2, "verify")
+    grp = LocalGroup(2, timeout_ms=30000)
+    engines = [grp.engine(r) for r in range(2)]
+    try:
+        def body(eng):
+            cfg = GnnConfig("x", H, 1, 1, mode="na2a" if eng.rank == 0 else "a2a")
+            eng.upload_graph(graphs[eng.rank])
+            eng.configure(cfg)
+            eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+            x0, e0, _ = gid_inputs(graphs[eng.rank], H)
+            with pytest.raises(CollectiveError):
+                eng.nmp_forward(x0, e0)
+            return True
+        assert grp.run(body, engines) == [True, True]
+    finally:
+        for e in engines:
+            e.close()
+        grp.close()
+
+
+def test_missing_rank_times_out(gpus):
+    """A rank that never enters the exchange fails its peer after the group
+    timeout instead of hanging it."""
+    E, p, H = 2, 2, 8
+    graphs = build_distributed_graph(E, p, 2, "verify")
+    cfg = GnnConfig("x", H, 1, 1, mode="na2a")
+    grp = LocalGroup(2, timeout_ms=1500)
+    engines = [grp.engine(r) for r in range(2)]
+    try:
+        def body(eng):
+            eng.upload_graph(graphs[eng.rank])
+            eng.configure(cfg)
+            eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+            if eng.rank == 1:
+                return "idle"
+            x0, e0, _ = gid_inputs(graphs[0], H)
+            with pytest.raises(CollectiveError, match="timeout"):
+                eng.nmp_forward(x0, e0)
+            return "raised"
+        assert grp.run(body, engines) == ["raised", "idle"]
+    finally:
+        for e in engines:
+            e.close()
+        grp.close()
