@@ -211,7 +211,14 @@ int hgnn_compute_gradients(hgnn_ctx* ctx, double* loss, double* grads, double* y
 int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double eps, double* loss);
 
 /* ---- options --------------------------------------------------------------- */
-/* "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
+/* "edge_factorized":  1 = (default, tcgen05 paths) the edge MLP's input linear is
+ *                     split through the nodes, P = x [W0_s | W0_d] once per node and
+ *                     only e W0_e per edge; the forward edge kernel also forms the
+ *                     aggregate (one fused kernel, no aggregate launch) and the
+ *                     backward's x adjoints / W0_s, W0_d gradients are node-level
+ *                     sums (no per-edge d_x_src / d_x_dst tensors). 0 = the
+ *                     3-segment edge kernels + aggregate + dx gather.
+ * "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
  *                     0 = SIMT fp32 kernels.
  * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
  *                      0 = SIMT fp32 kernels.
@@ -231,7 +238,9 @@ int hgnn_set_option(hgnn_ctx* ctx, const char* key, int64_t value);
 enum {
   HGNN_K_EDGE_FWD = 0, HGNN_K_EDGE_BWD = 1, HGNN_K_NODE_FWD = 2, HGNN_K_NODE_BWD = 3,
   HGNN_K_AGG = 4, HGNN_K_DX = 5, HGNN_K_HALO = 6, HGNN_K_GRAD_REDUCE = 7,
-  HGNN_K_ENCODE = 8, HGNN_K_DECODE = 9, HGNN_K_LOSS_ADAM = 10, HGNN_K_COUNT = 11
+  HGNN_K_ENCODE = 8, HGNN_K_DECODE = 9, HGNN_K_LOSS_ADAM = 10,
+  HGNN_K_EDGE_PROJ = 11, /* node-level projections P = x [W0_s | W0_d] of the factorised edge MLP */
+  HGNN_K_COUNT = 12
 };
 int hgnn_kernel_timing(hgnn_ctx* ctx, int enable);
 int hgnn_kernel_time(hgnn_ctx* ctx, int kernel_class, double* total_ms, int64_t* launches);

@@ -65,7 +65,8 @@ MODES = {"none": MODE_NONE, "a2a": MODE_A2A, "na2a": MODE_NA2A}
 PART_SLAB, PART_BLOCK, PART_VERIFY = 0, 1, 2
 TRACE_X_IN, TRACE_E_IN, TRACE_A_SYNC, TRACE_X_OUT, TRACE_E_OUT = range(5)
 K_EDGE_FWD, K_EDGE_BWD, K_NODE_FWD, K_NODE_BWD, K_AGG, K_DX, K_HALO, K_GRAD_REDUCE = range(8)
-KERNEL_CLASSES = ["edge_fwd", "edge_bwd", "node_fwd", "node_bwd", "aggregate", "dx_gather", "halo", "grad_reduce", "encode", "decode", "loss_adam"]
+KERNEL_CLASSES = ["edge_fwd", "edge_bwd", "node_fwd", "node_bwd", "aggregate", "dx_gather", "halo", "grad_reduce", "encode",
+                  "decode", "loss_adam", "edge_proj"]
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "edge_fact.cuh"
 #include "engine_ctx.hpp"
 #include "graph_kernels.cuh"
 #include "mlp_simt.cuh"
@@ -138,27 +139,6 @@ float tf32_rna_host(float x) {
 
 bool tc_eligible(const hgnn_ctx* c) { return c->H == 32 || c->H == 64; }
 
-// Chunks of one processor MLP in MMA order: the input linear split into
-// nseg K-chunks of H rows, then one chunk per H x H linear. Each chunk is the
-// B operand [W_hi | W_lo]^T (2H x H) in K-major core-matrix order.
-
-void build_chunks(const float* p, int in_dim, int H, int K, std::vector<float>& out) {
-  const int64_t base = (int64_t)out.size();
-  out.resize((size_t)(base + chunk_floats_fwd(in_dim, H, K)));
-  chunk_layout_fwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
-    const float hi = tf32_rna_host(p[src]);
-    out[(size_t)pos] = lo ? tf32_rna_host(p[src] - hi) : hi;
-  });
-}
-void build_bwd_chunks(const float* p, int in_dim, int H, int K, std::vector<float>& out) {
-  const int64_t base = (int64_t)out.size();
-  out.resize((size_t)(base + chunk_floats_bwd(in_dim, H, K)));
-  chunk_layout_bwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
-    const float hi = tf32_rna_host(p[src]);
-    out[(size_t)pos] = lo ? tf32_rna_host(p[src] - hi) : hi;
-  });
-}
-
 // --------------------------------------------------------------------------
 // buffers
 // --------------------------------------------------------------------------
@@ -200,6 +180,16 @@ void ensure_buffers(hgnn_ctx* c) {
   const int64_t n_slots = (2 * c->K + 1) * H + c->K;
   c->scratch.alloc(max_grid * n_slots * kMlpThreads);
   if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
+  if (c->ps.size() != (size_t)M || (M > 0 && c->ps[0]->n != c->rows * 2 * H)) {
+    c->ps.clear();
+    for (int64_t m = 0; m < M; ++m) {
+      c->ps.emplace_back(new DevBuf<float>());
+      if (c->edge_fact && c->fact_ok && tc_eligible(c)) c->ps.back()->alloc(c->rows * 2 * H);
+    }
+  }
+  if (c->ps_ready.size() != (size_t)M) c->ps_ready.assign((size_t)M, 0);
+  c->fact_blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (c->rows + 15) / 16), (int64_t)c->num_sms * 4);
+  if (c->edge_fact && c->fact_ok && tc_eligible(c)) c->fact_part.alloc((int64_t)c->fact_blocks * 2 * H * H);
   c->stage_elems = std::min<int64_t>(std::max<int64_t>(c->rows, c->ne) * H, int64_t{1} << 24);
   c->stage.alloc(std::max<int64_t>(c->stage_elems, 1));
   // halo buffers
@@ -530,7 +520,7 @@ void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const f
   args.e_in = e ? e + s0 * c->H : nullptr;
   args.a = a;
   args.out = out + s0 * c->H;
-  args.chunks = c->chunks.p + c->chunk_off[(size_t)(2 * m + (edge ? 0 : 1))];
+  args.chunks = c->chunks.p + c->chunk_off[(size_t)(3 * m + (edge ? 0 : 1))];
   args.params = layer_params(c, m, edge).p;
   args.k = (int)c->K;
   args.prof = c->prof_on ? c->prof.p + 2 * kProfCount + (edge ? 0 : kProfCount) : nullptr;
@@ -543,7 +533,59 @@ void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const f
   }
 }
 
+bool use_fact(const hgnn_ctx* c) { return c->edge_fact && c->fact_ok && tc_eligible(c); }
+bool use_fact_fwd(const hgnn_ctx* c) { return use_tc(c) && use_fact(c); }
+
+// P_m = x_m [W0_s | W0_d] on the local rows (edges never reference halo rows)
+void edge_proj(hgnn_ctx* c, int64_t m, const float* x) {
+  Timed t(c, HGNN_K_EDGE_PROJ);
+  if (c->nl == 0) return;
+  const float* w0 = layer_params(c, m, true).p;
+  const unsigned grid = (unsigned)std::min<int64_t>((c->nl + 15) / 16, (int64_t)c->num_sms * 8);
+  if (c->H == 64) edge_proj_kernel<64><<<grid, kFactThreads, 0, c->stream>>>(x, w0, c->nl, c->ps[(size_t)m]->p);
+  else edge_proj_kernel<32><<<grid, kFactThreads, 0, c->stream>>>(x, w0, c->nl, c->ps[(size_t)m]->p);
+  check_launch(c);
+  c->ps_ready[(size_t)m] = 1;
+}
+
+// The fused edge update (kEdgeFact): tiles [t0, t1) of the segment table;
+// writes e' (es[m + 1]) and the aggregate of every receiver in those tiles.
+template <int H>
+void launch_fact_typed(hgnn_ctx* c, const TcFwdArgs& args) {
+  auto k = mlp_tc_forward_kernel<H, kEdgeFact, false>;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<H>::SMEM_FACT));
+  const int64_t pairs = (args.n_tiles + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms - c->sm_reserve));
+  k<<<grid, TcCfg<H>::THREADS, TcCfg<H>::SMEM_FACT, c->stream>>>(args);
+  check_launch(c);
+}
+void launch_fact_forward(hgnn_ctx* c, int64_t m, int64_t t0, int64_t t1, const float* e, float* e2, float* a) {
+  if (t1 <= t0) return;
+  TcFwdArgs args{};
+  args.n_tiles = t1 - t0;
+  args.tiles = c->tiles.p + t0;
+  args.src = c->src.p;
+  args.dst = c->dst.p;
+  args.inv = c->inv.p;
+  args.e_in = e;
+  args.out = e2;
+  args.agg = a;
+  args.proj = c->ps[(size_t)m]->p;
+  args.chunks = c->chunks.p + c->chunk_off[(size_t)(3 * m + 2)];
+  args.params = layer_params(c, m, true).p;
+  args.k = (int)c->K;
+  if (c->H == 64) launch_fact_typed<64>(c, args);
+  else launch_fact_typed<32>(c, args);
+}
+void zero_empty_rows(hgnn_ctx* c, float* a) {
+  if (c->n_rows_empty == 0) return;
+  zero_rows_kernel<<<blocks_for(c->n_rows_empty * c->H / 4), kEwThreads, 0, c->stream>>>(c->rows_empty.p,
+                                                                                       c->n_rows_empty, (int)c->H, a);
+  check_launch(c);
+}
+
 bool use_tc_bwd(const hgnn_ctx* c) { return c->bwd_impl == 1 && c->H == 64; }
+bool use_fact_bwd(const hgnn_ctx* c) { return use_tc_bwd(c) && use_fact(c); }
 
 int tc_bwd_grid(const hgnn_ctx* c, int64_t n_rows) {
   const int64_t pairs = ((n_rows + 127) / 128 + 1) / 2;
@@ -552,17 +594,19 @@ int tc_bwd_grid(const hgnn_ctx* c, int64_t n_rows) {
 
 // Returns the grid used (rows of grad_part written).
 int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
-  const bool edge = mode == kEdgeInput;
+  const bool edge = mode != kNodeInput;
   TcBwdArgs args = in;
-  args.chunks = c->bchunks.p + c->bchunk_off[(size_t)(2 * m + (edge ? 0 : 1))];
+  args.chunks = c->bchunks.p + c->bchunk_off[(size_t)(3 * m + (mode == kEdgeFact ? 2 : (edge ? 0 : 1)))];
   args.params = layer_params(c, m, edge).p;
   args.k = (int)c->K;
   args.scratch = c->tc_scratch.p;
   args.prof = c->prof_on ? c->prof.p + (edge ? 0 : kProfCount) : nullptr;
   const int grid = tc_bwd_grid(c, args.n_rows);
   const bool prof = args.prof != nullptr;
-  auto k = edge ? (prof ? mlp_tc_backward_kernel<kEdgeInput, true> : mlp_tc_backward_kernel<kEdgeInput, false>)
-                : (prof ? mlp_tc_backward_kernel<kNodeInput, true> : mlp_tc_backward_kernel<kNodeInput, false>);
+  auto k = mode == kEdgeFact
+               ? (prof ? mlp_tc_backward_kernel<kEdgeFact, true> : mlp_tc_backward_kernel<kEdgeFact, false>)
+               : edge ? (prof ? mlp_tc_backward_kernel<kEdgeInput, true> : mlp_tc_backward_kernel<kEdgeInput, false>)
+                      : (prof ? mlp_tc_backward_kernel<kNodeInput, true> : mlp_tc_backward_kernel<kNodeInput, false>);
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
   k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(args);
   check_launch(c);
@@ -587,6 +631,55 @@ void node_forward(hgnn_ctx* c, int64_t m, const float* x, const float* a, float*
 }
 
 
+void sync_aggregates(hgnn_ctx* c, float* a) {
+  if (c->n_sync == 0) return;
+  Timed t(c, HGNN_K_HALO);
+  sync_kernel<<<blocks_for(c->n_sync * c->H / 4), kEwThreads, 0, c->stream>>>(a, c->sync_local.p, c->sync_off.p,
+                                                                              c->sync_slots.p, c->n_sync, (int)c->H);
+  check_launch(c);
+}
+
+bool can_overlap(const hgnn_ctx* c) {
+  return c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group);
+}
+
+// Edge update of the factorised MP layer: node projections, then ONE fused
+// kernel (gather -> tcgen05 MLP -> e' + segmented 1/d aggregate); with an
+// exchange, the boundary tiles first and the exchange on the side stream
+// while the interior tiles run.
+void layer_forward_fact(hgnn_ctx* c, int64_t m, float* x, float* e, float* e2, float* a, float* x2) {
+  edge_proj(c, m, x);
+  zero_empty_rows(c, a);  // empty segments (halo rows: before the receive overwrites them)
+  if (can_overlap(c) && c->n_tiles_bnd > 0) {
+    {
+      Timed t(c, HGNN_K_EDGE_FWD);
+      launch_fact_forward(c, m, 0, c->n_tiles_bnd, e, e2, a);
+    }
+    CUDA_OK(cudaEventRecord(c->ev_bnd, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_bnd, 0));
+    halo_exchange(c, a, c->side);
+    CUDA_OK(cudaEventRecord(c->ev_halo, c->side));
+    {
+      Timed t(c, HGNN_K_EDGE_FWD);
+      c->sm_reserve = c->halo_sm_reserve;
+      launch_fact_forward(c, m, c->n_tiles_bnd, c->n_tiles, e, e2, a);
+      c->sm_reserve = 0;
+    }
+    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    sync_aggregates(c, a);
+  } else {
+    {
+      Timed t(c, HGNN_K_EDGE_FWD);
+      launch_fact_forward(c, m, 0, c->n_tiles, e, e2, a);
+    }
+    if (c->mode != HGNN_MODE_NONE) {
+      halo_exchange(c, a, c->stream);
+      sync_aggregates(c, a);
+    }
+  }
+  node_forward(c, m, x, a, x2);
+}
+
 void layer_forward(hgnn_ctx* c, int64_t m) {
   const int64_t H = c->H;
   float* x = c->xs[m]->p;
@@ -594,6 +687,10 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   float* e2 = c->es[m + 1]->p;
   float* a = c->as[m]->p;
   float* x2 = c->xs[m + 1]->p;
+  if (use_fact_fwd(c)) {
+    layer_forward_fact(c, m, x, e, e2, a, x2);
+    return;
+  }
   if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group) && c->n_rows_bnd > 0 &&
       use_tc(c)) {
     // Overlapped schedule, same results: boundary-row edges + aggregates,
@@ -716,6 +813,9 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       if (c->nl > 0) reduce_grads(c, c->grid_node_b, c->n_node_par, c->grads.p + goff + c->n_edge_par);
     }
   }
+  const bool fact = use_fact_bwd(c);
+  const int emode = fact ? kEdgeFact : kEdgeInput;
+  if (fact && !c->ps_ready[(size_t)m]) edge_proj(c, m, x);  // forward ran without the node projections
   if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group) && c->n_rows_bnd > 0 &&
       use_tc_bwd(c)) {
     // Overlapped schedule: sync adjoint, then the adjoint exchange on the side
@@ -748,6 +848,8 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.de_io = c->de.p + s0 * H;
       args.d_src = c->dsrc.p + s0 * H;
       args.d_dst = c->ddst.p + s0 * H;
+      args.proj = fact ? c->ps[(size_t)m]->p : nullptr;
+      args.dy_out = c->dsrc.p + s0 * H;  // kEdgeFact: dY
       args.grad_partial = part;
       return args;
     };
@@ -757,7 +859,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
                               c->stream));
       if (n_int > 0) {
         c->sm_reserve = c->halo_sm_reserve;
-        launch_tc_backward(c, kEdgeInput, m, edge_args(c->ne_bnd, n_int, c->grad_part.p));
+        launch_tc_backward(c, emode, m, edge_args(c->ne_bnd, n_int, c->grad_part.p));
         c->sm_reserve = 0;
       }
     }
@@ -765,7 +867,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
     {
       Timed t(c, HGNN_K_EDGE_BWD);
       if (c->ne_bnd > 0)
-        launch_tc_backward(c, kEdgeInput, m, edge_args(0, c->ne_bnd, c->grad_part.p + 2 * g1 * c->n_edge_par));
+        launch_tc_backward(c, emode, m, edge_args(0, c->ne_bnd, c->grad_part.p + 2 * g1 * c->n_edge_par));
       reduce_grads(c, 2 * (g1 + g2), c->n_edge_par, c->grads.p + goff);
     }
   } else {
@@ -794,9 +896,11 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.de_io = c->de.p;
       args.d_src = c->dsrc.p;
       args.d_dst = c->ddst.p;
+      args.proj = fact ? c->ps[(size_t)m]->p : nullptr;
+      args.dy_out = c->dsrc.p;  // kEdgeFact: dY
       args.grad_partial = c->grad_part.p;
       if (c->ne > 0) {
-        launch_tc_backward(c, kEdgeInput, m, args);
+        launch_tc_backward(c, emode, m, args);
         reduce_grads(c, 2 * grid, c->n_edge_par, c->grads.p + goff);
       }
     } else {
@@ -820,7 +924,21 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
     }
   }
   }  // serial schedule
-  {  // input-node adjoint (model.cpp:378-386)
+  if (fact) {  // input-node adjoint through the node-level sums of dY (edge_fact.cuh), + dW0_s / dW0_d
+    Timed t(c, HGNN_K_DX);
+    const float* w0 = layer_params(c, m, true).p;
+    if (H == 64)
+      edge_input_adjoint_kernel<64><<<c->fact_blocks, kFactThreads, 0, c->stream>>>(
+          c->dsrc.p, x, c->dxn.p, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
+    else
+      edge_input_adjoint_kernel<32><<<c->fact_blocks, kFactThreads, 0, c->stream>>>(
+          c->dsrc.p, x, c->dxn.p, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
+    check_launch(c);
+    const int64_t nw = 2 * H * H;  // W0 rows 0 .. 2H-1 (x_src, x_dst blocks) of the edge MLP
+    grad_reduce_add_kernel<<<blocks_for(nw), kEwThreads, 0, c->stream>>>(c->fact_part.p, c->fact_blocks, nw,
+                                                                         c->grads.p + goff);
+    check_launch(c);
+  } else {  // input-node adjoint (model.cpp:378-386)
     Timed t(c, HGNN_K_DX);
     dx_gather_kernel<<<blocks_for(c->rows * H / 4), kEwThreads, 0, c->stream>>>(
         c->dsrc.p, c->ddst.p, c->dxn.p, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, (int)H, c->dx.p);
@@ -829,6 +947,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
 }
 
 void run_forward(hgnn_ctx* c) {
+  c->ps_ready.assign((size_t)c->M, 0);
   for (int64_t m = 0; m < c->M; ++m) layer_forward(c, m);
   c->forward_done = true;
 }
@@ -895,8 +1014,9 @@ int hgnn_ctx_create_local(int device, int32_t rank, hgnn_local_group* group, hgn
     LocalGroup* G = reinterpret_cast<LocalGroup*>(group);
     if (rank < 0 || rank >= G->R) fail(HGNN_ERR_CONFIG, "hgnn_ctx_create_local: bad rank");
     hgnn_ctx* c = nullptr;
-    const int rc = hgnn_ctx_create(device, rank, 1, nullptr, &c);
+    const int rc = hgnn_ctx_create(device, 0, 1, nullptr, &c);  // a single-rank context, then joined to the group
     if (rc != HGNN_OK) fail(rc, hgnn_last_error());
+    c->rank = rank;
     c->nranks = G->R;
     c->group = G;
     try {
@@ -1053,6 +1173,44 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
     c->n_rows_int = split ? (int64_t)ri.size() : 0;
     c->rows_bnd.upload(rb.data(), c->n_rows_bnd, c->stream);
     c->rows_int.upload(ri.data(), c->n_rows_int, c->stream);
+    {  // fused edge kernel tiles: runs of whole receiver segments, <= 128 slots,
+       // in slot order, cut at the boundary / interior split
+      std::vector<int32_t> tl{0}, empty;
+      int32_t cur = 0;  // slots in the open tile
+      bool ok = true;
+      auto add_rows = [&](const std::vector<int32_t>& order) {
+        for (int32_t i : order) {
+          const int32_t len = seg_e[(size_t)i] - seg_b[(size_t)i];
+          if (len == 0) {
+            empty.push_back(i);
+            continue;
+          }
+          if (len > 128) ok = false;
+          if (cur + len > 128 && cur > 0) {
+            tl.push_back(seg_b[(size_t)i]);
+            cur = 0;
+          }
+          cur += len;
+        }
+        if (cur > 0) {
+          tl.push_back(tl.back() + cur);
+          cur = 0;
+        }
+      };
+      std::vector<int32_t> all_rows;
+      if (!split) {
+        all_rows.resize((size_t)rows);
+        for (int64_t i = 0; i < rows; ++i) all_rows[(size_t)i] = (int32_t)i;
+      }
+      add_rows(split ? rb : all_rows);
+      c->n_tiles_bnd = split ? (int64_t)tl.size() - 1 : 0;
+      if (split) add_rows(ri);
+      c->fact_ok = ok && tl.back() == ne;
+      c->n_tiles = (int64_t)tl.size() - 1;
+      c->tiles.upload(tl.data(), (int64_t)tl.size(), c->stream);
+      c->n_rows_empty = (int64_t)empty.size();
+      c->rows_empty.upload(empty.data(), c->n_rows_empty, c->stream);
+    }
     std::vector<int64_t> gids(g->global_ids, g->global_ids + rows);
     c->gid.upload(gids.data(), rows, c->stream);
     // halo map
@@ -1202,30 +1360,21 @@ int hgnn_params_upload(hgnn_ctx* c, const double* flat, int64_t count) {
     c->par.upload(p.data(), count, c->stream);
     c->par_t.upload(pt.data(), count, c->stream);
     if (tc_eligible(c)) {
-      std::vector<float> ch;
-      c->chunk_off.clear();
-      int64_t poff = 0;
-      for (int64_t m = 0; m < c->M; ++m)
-        for (int which = 0; which < 2; ++which) {
-          const int in_dim = (which == 0 ? 3 : 2) * H;
-          c->chunk_off.push_back((int64_t)ch.size());
-          build_chunks(p.data() + poff, in_dim, H, K, ch);
-          poff += mlp_param_count(in_dim, H, K);
-        }
-      c->chunks.upload(ch.data(), (int64_t)ch.size(), c->stream);
-    }
-    if (H == 64) {
-      std::vector<float> ch;
-      c->bchunk_off.clear();
-      int64_t poff = 0;
-      for (int64_t m = 0; m < c->M; ++m)
-        for (int which = 0; which < 2; ++which) {
-          const int in_dim = (which == 0 ? 3 : 2) * H;
-          c->bchunk_off.push_back((int64_t)ch.size());
-          build_bwd_chunks(p.data() + poff, in_dim, H, K, ch);
-          poff += mlp_param_count(in_dim, H, K);
-        }
-      c->bchunks.upload(ch.data(), (int64_t)ch.size(), c->stream);
+      std::vector<float> ch, bch;
+      int64_t nf = 0, nb = 0;
+      const bool with_bwd = H == 64;
+      mp_chunk_plan(H, K, c->M, with_bwd, [](bool, int64_t, int64_t, bool) {}, c->chunk_off, c->bchunk_off, nf, nb);
+      ch.resize((size_t)nf);
+      bch.resize((size_t)nb);
+      mp_chunk_plan(
+          H, K, c->M, with_bwd,
+          [&](bool fwd, int64_t pos, int64_t src, bool lo) {
+            const float hi = tf32_rna_host(p[(size_t)src]);
+            (fwd ? ch : bch)[(size_t)pos] = lo ? tf32_rna_host(p[(size_t)src] - hi) : hi;
+          },
+          c->chunk_off, c->bchunk_off, nf, nb);
+      c->chunks.upload(ch.data(), nf, c->stream);
+      c->bchunks.upload(bch.data(), nb, c->stream);
     }
     c->grads.alloc(std::max<int64_t>(count, 1));
     CUDA_OK(cudaStreamSynchronize(c->stream));
@@ -1356,6 +1505,10 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
     } else if (k == "halo_sm_reserve") {
       if (value < 0 || value > 32) fail(HGNN_ERR_CONFIG, "halo_sm_reserve: 0..32 SMs");
       c->halo_sm_reserve = (int)value;
+    } else if (k == "edge_factorized") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "edge_factorized: 0 (3-segment edge kernels) or 1");
+      if (c->edge_fact != (int)value) c->ps.clear();  // (re)allocated by ensure_buffers
+      c->edge_fact = (int)value;
     } else if (k == "mlp_backward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
       c->bwd_impl = (int)value;

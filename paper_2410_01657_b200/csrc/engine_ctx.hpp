@@ -107,7 +107,7 @@ struct hgnn_ctx {
   int64_t n_edge_par = 0, n_node_par = 0, n_mp_par = 0;
   hgnn_b200::DevBuf<float> par, par_t;
   hgnn_b200::DevBuf<float> chunks;                 // tcgen05 B operands, [W_hi | W_lo]^T chunks per MLP
-  std::vector<int64_t> chunk_off;       // per (layer, edge/node)
+  std::vector<int64_t> chunk_off;       // per (layer, edge / node / factorised edge): mp_chunk_plan
   hgnn_b200::DevBuf<double> grads;
   int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
   int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
@@ -116,6 +116,18 @@ struct hgnn_ctx {
   hgnn_b200::DevBuf<float> tc_scratch;
   hgnn_b200::DevBuf<unsigned long long> prof;      // optional backward-kernel wait profile
   bool prof_on = false;
+
+  // factorised edge MLP (kEdgeFact, edge_fact.cuh): receiver-segment tiles of
+  // the fused edge kernel ([0, n_tiles_bnd) cover the boundary slots), rows
+  // with an empty segment (zeroed aggregate), node projections per layer
+  int edge_fact = 1;              // option "edge_factorized"
+  bool fact_ok = false;           // every receiver segment fits one 128-slot tile
+  hgnn_b200::DevBuf<int32_t> tiles, rows_empty;
+  int64_t n_tiles = 0, n_tiles_bnd = 0, n_rows_empty = 0;
+  std::vector<std::unique_ptr<hgnn_b200::DevBuf<float>>> ps;  // P_m = x_m [W0_s | W0_d], rows x 2H
+  std::vector<uint8_t> ps_ready;                              // P_m computed by this forward
+  hgnn_b200::DevBuf<float> fact_part;                         // node-level dW0_s / dW0_d partials
+  int fact_blocks = 0;
 
   // activations
   std::vector<std::unique_ptr<hgnn_b200::DevBuf<float>>> xs, es, as;
@@ -190,15 +202,19 @@ struct Timed {
 // element `src` of the MLP's for_each parameter block at chunk float `pos`,
 // as its tf32 hi part (lo = false) or lo part (lo = true).
 // Forward sequence (mlp_tc.cuh): input segments of W0, W1 .. W_{k+1}.
+// seg0 / nseg: the input segments (K = H row blocks of W0) the kernel
+// multiplies on the tensor cores: all of them, or only the e block (seg0 = 2,
+// nseg = 1) for the factorised edge MLP (kEdgeFact).
 template <class Emit>
-void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
-  const int nseg = in_dim / H;
+void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int seg0 = 0, int nseg = -1) {
+  if (nseg < 0) nseg = in_dim / H;
   for (int l = 0; l < K + 2; ++l) {
     const int64_t w = mlp_w_offset(l, in_dim, H);
     const int n_ch = l == 0 ? nseg : 1;
-    for (int cidx = 0; cidx < n_ch; ++cidx, base += 2 * (int64_t)H * H)
+    for (int ci = 0; ci < n_ch; ++ci, base += 2 * (int64_t)H * H)
       for (int kk = 0; kk < H; ++kk)
         for (int n = 0; n < H; ++n) {
+          const int cidx = l == 0 ? seg0 + ci : 0;
           const int64_t src = w + (int64_t)(cidx * H + kk) * H + n;
           emit(base + tc_chunk_index(n, kk, H), src, false);
           emit(base + tc_chunk_index(H + n, kk, H), src, true);
@@ -210,8 +226,8 @@ void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
 // per input segment. A transposed chunk stores element (n = input feature,
 // k = output feature) = W[n][k].
 template <class Emit>
-void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
-  const int nseg = in_dim / H;
+void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int seg0 = 0, int nseg = -1) {
+  if (nseg < 0) nseg = in_dim / H;
   auto chunk = [&](auto src_of) {
     for (int kk = 0; kk < H; ++kk)
       for (int n = 0; n < H; ++n) {
@@ -222,13 +238,51 @@ void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit) {
     base += 2 * (int64_t)H * H;
   };
   auto W = [&](int l) { return mlp_w_offset(l, in_dim, H); };
-  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + kk) * H + n; });
+  for (int c = seg0; c < seg0 + nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + kk) * H + n; });
   for (int l = 1; l <= K; ++l) chunk([&](int n, int kk) { return W(l) + (int64_t)kk * H + n; });
   for (int l = K + 1; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * H + kk; });
-  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + n) * H + kk; });
+  for (int c = seg0; c < seg0 + nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + n) * H + kk; });
 }
-inline int64_t chunk_floats_fwd(int in_dim, int H, int K) { return (int64_t)(in_dim / H + K + 1) * 2 * H * H; }
-inline int64_t chunk_floats_bwd(int in_dim, int H, int K) { return (int64_t)(2 * (in_dim / H) + 2 * K + 1) * 2 * H * H; }
+inline int64_t chunk_floats_fwd(int in_dim, int H, int K, int nseg = -1) {
+  return (int64_t)((nseg < 0 ? in_dim / H : nseg) + K + 1) * 2 * H * H;
+}
+inline int64_t chunk_floats_bwd(int in_dim, int H, int K, int nseg = -1) {
+  return (int64_t)(2 * (nseg < 0 ? in_dim / H : nseg) + 2 * K + 1) * 2 * H * H;
+}
+
+// Every tcgen05 weight-chunk sequence of the MP block, in buffer order: per
+// layer m the edge MLP (3 input segments), the node MLP, and the factorised
+// edge MLP (kEdgeFact: e segment only); fwd offsets at [3 m + {0, 1, 2}], the
+// backward sequences (H = 64) likewise. emit(fwd?, pos, src, lo) places
+// element src of the MP parameter block; the same code serves the host upload
+// and the device refresh maps of the Adam step.
+template <class Emit>
+void mp_chunk_plan(int H, int K, int64_t M, bool with_bwd, Emit&& emit, std::vector<int64_t>& fwd_off,
+                   std::vector<int64_t>& bwd_off, int64_t& fwd_total, int64_t& bwd_total) {
+  fwd_off.clear();
+  bwd_off.clear();
+  fwd_total = bwd_total = 0;
+  int64_t off = 0;
+  for (int64_t m = 0; m < M; ++m) {
+    const int64_t off_edge = off, off_node = off + mlp_param_count(3 * H, H, K);
+    for (int v = 0; v < 3; ++v) {
+      const int in_dim = (v == 1 ? 2 : 3) * H;
+      const int seg0 = v == 2 ? 2 : 0, nseg = v == 2 ? 1 : -1;
+      const int64_t poff = v == 1 ? off_node : off_edge;
+      fwd_off.push_back(fwd_total);
+      chunk_layout_fwd(in_dim, H, K, fwd_total, [&](int64_t pos, int64_t src, bool lo) { emit(true, pos, poff + src, lo); },
+                       seg0, nseg);
+      fwd_total += chunk_floats_fwd(in_dim, H, K, nseg);
+      if (with_bwd) {
+        bwd_off.push_back(bwd_total);
+        chunk_layout_bwd(in_dim, H, K, bwd_total,
+                         [&](int64_t pos, int64_t src, bool lo) { emit(false, pos, poff + src, lo); }, seg0, nseg);
+        bwd_total += chunk_floats_bwd(in_dim, H, K, nseg);
+      }
+    }
+    off = off_node + mlp_param_count(2 * H, H, K);
+  }
+}
 
 void bind(hgnn_ctx* c);
 // in-place sum over ranks of n device doubles on the compute stream (NCCL, or

@@ -17,6 +17,16 @@
 // The two slots ping-pong: the MMA of one tile runs while the other tile's
 // epilogue works. Input rows (x[src], x[dst], e / a*, x) are gathered one
 // segment ahead so their latency hides behind the MMA of the previous one.
+//
+// kEdgeFact (the edge update of the MP layer, model.cpp:233-240, as ONE
+// kernel): tiles are runs of whole receiver segments (<= 128 slots, from a
+// table built at graph upload); the input linear is one K = H segment
+// (e W0_e) plus the gathered node projections P_s[src] + P_d[dst]; the output
+// rows go through a swizzled shared-memory tile to a reducer warp per slot
+// (warps 10 / 11) that streams e' to HBM with coalesced row stores and forms
+// the degree-scaled aggregate a[i] = sum inv_d e' over each receiver segment
+// in slot order (= scatter_rows_csr's in-CSR order, kernels.cpp:355-368), so
+// e' is never re-read and no atomics are used.
 #pragma once
 
 #include "mlp_simt.cuh"
@@ -36,7 +46,11 @@ struct TcCfg {
   static constexpr int TMEM_COLS = H == 64 ? 512 : 256;  // power of two >= 2 slots
   static constexpr int STAGES = H == 64 ? 4 : 8;
   static constexpr int THREADS = 384;  // 2 epilogue warpgroups + 1 control warpgroup
-  static constexpr size_t SMEM = (size_t)STAGES * CHUNK_BYTES + 1024 + 256 + 18 * H * 4;  // + biases (k <= 16)
+  static constexpr size_t OFF_BARS = (size_t)STAGES * CHUNK_BYTES;
+  static constexpr size_t OFF_BIAS = OFF_BARS + 256;
+  static constexpr size_t OFF_Y = OFF_BIAS + 18 * H * 4;              // kEdgeFact: 2 output tiles (128 x H)
+  static constexpr size_t SMEM = OFF_Y + 1024;                         // + biases (k <= 16)
+  static constexpr size_t SMEM_FACT = OFF_Y + 2 * 128 * H * 4 + 1024;
 };
 
 // Index (in floats) of B element (n, k) inside a chunk (K-major core matrices).
@@ -57,6 +71,12 @@ struct TcFwdArgs {
   const float* params;  // fp32 for_each layout (biases)
   int k;
   unsigned long long* prof;  // optional cycle counters (kFwdProf*), PROF instantiation only
+  // kEdgeFact
+  int64_t n_tiles;
+  const int32_t* tiles;  // [n_tiles + 1] slot offsets; tile t = slots [tiles[t], tiles[t+1])
+  const float* proj;     // rows x 2H: [P_s | P_d] = x [W0_s | W0_d]
+  const float* inv;      // per slot 1/d
+  float* agg;            // rows x H aggregate (rows with an empty segment are not written)
 };
 
 // Optional instrumentation of the forward kernel (cycles summed over CTAs;
@@ -104,7 +124,7 @@ __device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const f
     float hi[32], lo[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      hi[j] = ptx::tf32_trunc(v[c + j]);
+      hi[j] = ptx::tf32_hi(v[c + j]);
       lo[j] = v[c + j] - hi[j];
     }
     ptx::tmem_st32(t_hi + c, hi);
@@ -136,7 +156,9 @@ template <int H, int MODE>
 __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool valid, int c, float (&v)[H]) {
   if (valid) {
     const float* seg;
-    if (MODE == kEdgeInput)
+    if (MODE == kEdgeFact)
+      seg = a.e_in + row * H;
+    else if (MODE == kEdgeInput)
       seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * H
                    : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
     else
@@ -155,28 +177,70 @@ __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool 
   }
 }
 
+// v = P_s[src[row]] + P_d[dst[row]] (kEdgeFact input projection of the node ends)
+template <int H>
+__device__ __forceinline__ void tc_gather_proj(const TcFwdArgs& a, int64_t row, bool valid, float (&v)[H]) {
+  if (!valid) {
+#pragma unroll
+    for (int j = 0; j < H; ++j) v[j] = 0.f;
+    return;
+  }
+  const float4* ps = reinterpret_cast<const float4*>(a.proj + (int64_t)__ldg(a.src + row) * (2 * H));
+  const float4* pd = reinterpret_cast<const float4*>(a.proj + (int64_t)__ldg(a.dst + row) * (2 * H) + H);
+#pragma unroll
+  for (int j = 0; j < H / 4; ++j) {
+    const float4 s = __ldg(ps + j), d = __ldg(pd + j);
+    v[4 * j] = s.x + d.x;
+    v[4 * j + 1] = s.y + d.y;
+    v[4 * j + 2] = s.z + d.z;
+    v[4 * j + 3] = s.w + d.w;
+  }
+}
+
+// Byte offset of 16-byte chunk c of row r in a 128 x H fp32 tile (chunk index
+// XOR row % 8: conflict-free row writes by row-per-thread warps and
+// conflict-free row reads by column-per-lane warps).
+template <int H>
+__device__ __forceinline__ uint32_t ytile_off(int r, int c) {
+  return (uint32_t)(r * H * 4 + ((c ^ (r & 7)) << 4));
+}
+
 template <int H, int MODE, bool PROF>
 __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(TcFwdArgs a) {
   using Cfg = TcCfg<H>;
-  constexpr int nseg = MODE == kEdgeInput ? 3 : 2;
-  constexpr int in_dim = nseg * H;
+  constexpr bool FACT = MODE == kEdgeFact;
+  constexpr int nseg = MODE == kEdgeInput ? 3 : (MODE == kNodeInput ? 2 : 1);
+  constexpr int in_dim = (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout (kEdgeFact: the 3H-input MLP)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* wring = reinterpret_cast<float*>(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)Cfg::STAGES * Cfg::CHUNK_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BARS);
   uint64_t* w_full = bars;                    // [STAGES]
   uint64_t* w_empty = bars + Cfg::STAGES;     // [STAGES]
   uint64_t* a_full = bars + 2 * Cfg::STAGES;  // [2]
   uint64_t* a_empty = a_full + 2;             // [2]
   uint64_t* d_full = a_empty + 2;             // [2]
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(d_full + 2);
-  float* sbias = reinterpret_cast<float*>(smem + (size_t)Cfg::STAGES * Cfg::CHUNK_BYTES + 256);  // (k+2) x H
+  uint64_t* y_full = d_full + 2;              // [2] kEdgeFact: output tile written (4 epilogue warps)
+  uint64_t* y_empty = y_full + 2;             // [2] kEdgeFact: output tile consumed (reducer warp)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(y_empty + 2);
+  float* sbias = reinterpret_cast<float*>(smem + Cfg::OFF_BIAS);  // (k+2) x H
+  uint8_t* ytile = smem + Cfg::OFF_Y;                             // kEdgeFact: [2][128][H] swizzled
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int n_chunks = nseg + a.k + 1;
-  const int64_t n_tiles = (a.n_rows + 127) / 128;
+  const int64_t n_tiles = FACT ? a.n_tiles : (a.n_rows + 127) / 128;
   const int64_t n_pairs = (n_tiles + 1) / 2;
+  // rows of tile t: [t_beg, t_end) (kEdgeFact: a run of whole receiver segments)
+  auto tile_rows = [&](int64_t t, int64_t& beg, int64_t& end) {
+    if (FACT) {
+      beg = t < n_tiles ? (int64_t)__ldg(a.tiles + t) : 0;
+      end = t < n_tiles ? (int64_t)__ldg(a.tiles + t + 1) : 0;
+    } else {
+      beg = t * 128;
+      end = beg + 128 < a.n_rows ? beg + 128 : a.n_rows;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -187,6 +251,8 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       ptx::mbar_init(&a_full[s], 4);
       ptx::mbar_init(&a_empty[s], 1);
       ptx::mbar_init(&d_full[s], 1);
+      ptx::mbar_init(&y_full[s], 4);
+      ptx::mbar_init(&y_empty[s], 1);
     }
     ptx::fence_mbarrier_init();
   }
@@ -225,14 +291,19 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       if (PROF) e_sig += (unsigned long long)(clock64() - t0);
     };
     float v[H];
+    const int trow = 32 * wq + lane;  // row inside the tile
+    uint32_t py = 0;                  // y_empty phase (kEdgeFact)
     int64_t pair = blockIdx.x;
     if (pair < n_pairs) {
-      const int64_t row0 = (2 * pair + g) * 128 + 32 * wq + lane;
-      tc_gather<H, MODE>(a, row0, row0 < a.n_rows, 0, v);
+      int64_t b0, e0;
+      tile_rows(2 * pair + g, b0, e0);
+      tc_gather<H, MODE>(a, b0 + trow, b0 + trow < e0, 0, v);
     }
     for (; pair < n_pairs; pair += gridDim.x) {
-      const int64_t row = (2 * pair + g) * 128 + 32 * wq + lane;
-      const bool valid = row < a.n_rows;
+      int64_t tb, te;
+      tile_rows(2 * pair + g, tb, te);
+      const int64_t row = tb + trow;
+      const bool valid = row < te;
       float h[H];
       const long long t_in0 = PROF ? clock64() : 0;
       // input projection: nseg K-chunks streamed through A, next one prefetched
@@ -249,8 +320,13 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         signal_a();
         if (c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v);
       }
+      if (FACT) tc_gather_proj<H>(a, row, valid, v);  // node-end projections, during the e W0_e MMA
       wait_d();
       tc_load_d<H>(t_d, sbias, h);
+      if (FACT) {
+#pragma unroll
+        for (int j = 0; j < H; ++j) h[j] += v[j];
+      }
       if (PROF) e_in += (unsigned long long)(clock64() - t_in0);
       // residual blocks
       for (int l = 1; l <= a.k; ++l) {
@@ -283,12 +359,32 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       signal_a();
       const int64_t next = pair + gridDim.x;
       if (next < n_pairs) {
-        const int64_t nrow = (2 * next + g) * 128 + 32 * wq + lane;
-        tc_gather<H, MODE>(a, nrow, nrow < a.n_rows, 0, v);
+        int64_t nb, ne_;
+        tile_rows(2 * next + g, nb, ne_);
+        tc_gather<H, MODE>(a, nb + trow, nb + trow < ne_, 0, v);
       }
       wait_d();
       const long long t_out0 = PROF ? clock64() : 0;
-      {  // stream y = D + b straight to global, 32 columns at a time
+      if (FACT) {  // y = D + b into this slot's output tile, for the reducer warp
+        const float* bo = sbias + (a.k + 1) * H;
+        ptx::mbar_wait(&y_empty[g], py ^ 1);  // previous tile of this slot consumed
+        py ^= 1;
+        uint8_t* yt = ytile + (size_t)g * 128 * H * 4;
+#pragma unroll
+        for (int c = 0; c < H; c += 32) {
+          float p[32];
+          ptx::tmem_ld32(t_d + c, p);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(yt + ytile_off<H>(trow, c / 4 + j)) =
+                make_float4(p[4 * j] + bo[c + 4 * j], p[4 * j + 1] + bo[c + 4 * j + 1],
+                            p[4 * j + 2] + bo[c + 4 * j + 2], p[4 * j + 3] + bo[c + 4 * j + 3]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&y_full[g]);
+      } else {  // stream y = D + b straight to global, 32 columns at a time
         const float* bo = sbias + (a.k + 1) * H;
         float4* o = reinterpret_cast<float4*>(a.out + row * H);
 #pragma unroll
@@ -373,6 +469,58 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         atomicAdd(a.prof + kFwdProfIssW, i_w);
         atomicAdd(a.prof + kFwdProfIssMma, i_m);
       }
+    }
+  } else if (FACT && warp >= 10) {
+    // ------------------------------------------------------------ reducer of slot g (warps 10, 11)
+    // e' rows to HBM (coalesced: the lanes cover one row) and the segment sums
+    // a[i] = sum_p inv[p] e'[p] in slot order (fmaf chain from 0, as
+    // aggregate_kernel): each receiver segment lies inside one tile.
+    const int g = warp - 10;
+    constexpr int CPL = H / 32;  // columns per lane
+    const uint8_t* yt = ytile + (size_t)g * 128 * H * 4;
+    uint32_t pf = 0;
+    for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+      int64_t tb, te;
+      tile_rows(2 * pair + g, tb, te);
+      const int n = (int)(te - tb);
+      ptx::mbar_wait(&y_full[g], pf);
+      pf ^= 1;
+      float acc[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
+      for (int r0 = 0; r0 < n; r0 += 32) {
+        const int rr = r0 + lane;
+        const int32_t d_l = rr < n ? __ldg(a.dst + tb + rr) : -1;
+        const int32_t dn_l = rr + 1 < n ? __ldg(a.dst + tb + rr + 1) : -1;
+        const float w_l = rr < n ? __ldg(a.inv + tb + rr) : 0.f;
+        const int cnt = n - r0 < 32 ? n - r0 : 32;
+        for (int i = 0; i < cnt; ++i) {
+          const int r = r0 + i;
+          const int32_t d = __shfl_sync(0xffffffffu, d_l, i);
+          const int32_t dn = __shfl_sync(0xffffffffu, dn_l, i);
+          const float w = __shfl_sync(0xffffffffu, w_l, i);
+          float* eo = a.out + (tb + r) * H + CPL * lane;
+          if (CPL == 2) {
+            const float2 y = *reinterpret_cast<const float2*>(yt + ytile_off<H>(r, lane / 2) + 8 * (lane & 1));
+            *reinterpret_cast<float2*>(eo) = y;
+            acc[0] = fmaf(w, y.x, acc[0]);
+            acc[CPL - 1] = fmaf(w, y.y, acc[CPL - 1]);
+          } else {
+            const float y = *reinterpret_cast<const float*>(yt + ytile_off<H>(r, lane / 4) + 4 * (lane & 3));
+            *eo = y;
+            acc[0] = fmaf(w, y, acc[0]);
+          }
+          if (dn != d) {  // last slot of receiver d's segment
+            float* ag = a.agg + (int64_t)d * H + CPL * lane;
+            if (CPL == 2) *reinterpret_cast<float2*>(ag) = make_float2(acc[0], acc[CPL - 1]);
+            else *ag = acc[0];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&y_empty[g]);
     }
   } else {
     // ------------------------------------------------------------ weight loader (warp 9; 10-11 idle)

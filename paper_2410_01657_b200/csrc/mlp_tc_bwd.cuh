@@ -76,6 +76,8 @@ struct TcBwdArgs {
   float* d_dst;
   float* d_a_out;        // node mode outputs
   float* d_x_out;
+  const float* proj;     // kEdgeFact: rows x 2H node projections [P_s | P_d] (recompute input)
+  float* dy_out;         // kEdgeFact: adjoint of the input linear's output (N_e x H), for the node-level sums
   const float* chunks;   // 2 nseg + 2k + 1 chunks in MMA order
   const float* params;   // fp32 for_each layout (biases)
   float* grad_partial;   // [gridDim.x][2][n_par]: (hh + hl, db) and lh partials
@@ -99,6 +101,13 @@ __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool
   f.a = a.a;
   tc_gather<64, MODE>(f, row, valid, c, v);
 }
+__device__ __forceinline__ void bwd_gather_proj(const TcBwdArgs& a, int64_t row, bool valid, float (&v)[64]) {
+  TcFwdArgs f{};
+  f.src = a.src;
+  f.dst = a.dst;
+  f.proj = a.proj;
+  tc_gather_proj<64>(f, row, valid, v);
+}
 
 // A <- [hi | lo] split of v, 16 columns at a time (low register pressure).
 __device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const float (&v)[64]) {
@@ -107,7 +116,7 @@ __device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const 
     float hi[16], lo[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      hi[j] = ptx::tf32_trunc(v[c + j]);
+      hi[j] = ptx::tf32_hi(v[c + j]);
       lo[j] = v[c + j] - hi[j];
     }
     ptx::tmem_st16(t_hi + c, hi);
@@ -176,10 +185,10 @@ __device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&
       x.w = sw ? v[4 * qb + 3] : v[4 * qa + 3];
       const int q = sw ? qb : qa;
       float4 hi, lo;
-      hi.x = ptx::tf32_trunc(x.x);
-      hi.y = ptx::tf32_trunc(x.y);
-      hi.z = ptx::tf32_trunc(x.z);
-      hi.w = ptx::tf32_trunc(x.w);
+      hi.x = ptx::tf32_hi(x.x);
+      hi.y = ptx::tf32_hi(x.y);
+      hi.z = ptx::tf32_hi(x.z);
+      hi.w = ptx::tf32_hi(x.w);
       lo.x = x.x - hi.x;
       lo.y = x.y - hi.y;
       lo.z = x.z - hi.z;
@@ -227,8 +236,11 @@ template <int MODE, bool PROF>
 __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(TcBwdArgs a) {
   using Cfg = TcBwdCfg;
   constexpr int H = Cfg::H;
-  constexpr int nseg = MODE == kEdgeInput ? 3 : 2;
-  constexpr int in_dim = nseg * H;
+  constexpr bool FACT = MODE == kEdgeFact;
+  constexpr bool EDGE = MODE != kNodeInput;
+  constexpr int nseg = MODE == kEdgeInput ? 3 : (MODE == kNodeInput ? 2 : 1);
+  constexpr int in_dim = (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout
+  constexpr int seg0 = FACT ? 2 : 0;                         // W0 row block of the first input segment
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* wring = reinterpret_cast<float*>(smem);
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const long long tf0 = PROF ? clock64() : 0;
       const int jj = (int)(jf % n_dw);
       const int lin = jj <= K ? K + 1 - jj : 0;
-      const int rowbase = jj <= K ? 0 : (jj - K - 1) * H;
+      const int rowbase = jj <= K ? 0 : (jj - K - 1 + seg0) * H;
       const bool with_db = jj <= K + 1;
       const int acc = (int)(jf & 1);
       ptx::mbar_wait(&dw_full[acc], (uint32_t)((jf >> 1) & 1));
@@ -404,10 +416,18 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         bwd_store_a(t_ahi, t_alo, h);
         tc_signal(&a_full[g]);
       }
+      if (FACT) bwd_gather_proj(a, row, valid, h);  // P_s[src] + P_d[dst], during the e W0_e MMA
       ptx::mbar_wait(&d_full[g], pd);
       pd ^= 1;
       ptx::tc_fence_after();
-      bwd_load_d(t_d, sbias, h);
+      if (FACT) {
+        float u[H];
+        bwd_load_d(t_d, sbias, u);
+#pragma unroll
+        for (int j = 0; j < H; ++j) h[j] += u[j];  // (D + b0) + proj, the forward's order
+      } else {
+        bwd_load_d(t_d, sbias, h);
+      }
       for (int l = 1; l <= K; ++l) {
         bwd_store_a(t_ahi, t_alo, h);
         tc_signal(&a_full[g]);
@@ -429,7 +449,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       // ---------------------------------------------- backward
       float dh[H];
       if (valid) {
-        if (MODE == kEdgeInput) {  // d_y = de + inv_d * d_a[dst] (model.cpp:354-360)
+        if (EDGE) {  // d_y = de + inv_d * d_a[dst] (model.cpp:354-360)
           const float s = __ldg(a.inv_deg + row);
           const float4* da = reinterpret_cast<const float4*>(a.d_a + (int64_t)__ldg(a.dst + row) * H);
           const float4* de = reinterpret_cast<const float4*>(a.de_io + row * H);
@@ -521,6 +541,12 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           tc_signal(&a_full[g]);
           write_db(dh);
         }
+        if (FACT && c == 0 && valid) {  // dY: the input linear's output adjoint, for the node-level sums
+          float4* o = reinterpret_cast<float4*>(a.dy_out + row * H);
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            ptx::st_hint(o + q, make_float4(dh[4 * q], dh[4 * q + 1], dh[4 * q + 2], dh[4 * q + 3]), once);
+        }
         if (c >= 0) bwd_gather<MODE>(a, row, valid, c, h);  // dW0 segment operand
         stage_chunk(h, dh);
         wait_dx();
@@ -529,7 +555,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           bwd_load_d(t_d, nullptr, dh);  // d_prev = d_u W^T + d_h
         } else {
           float* outp;
-          if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
+          if (FACT) outp = a.de_io;
+          else if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
           else outp = c == 0 ? a.d_a_out : a.d_x_out;
           float4* o = reinterpret_cast<float4*>(outp + row * H);
 #pragma unroll

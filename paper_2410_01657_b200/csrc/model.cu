@@ -177,22 +177,21 @@ void build_refresh_maps(hgnn_ctx* c) {
           for (int j = 0; j < H; ++j) pt[(size_t)(wo + (int64_t)j * rin + i)] = (int32_t)(wo + (int64_t)i * H + j);
         for (int j = 0; j < H; ++j) pt[(size_t)(bo + j)] = (int32_t)(bo + j);
       }
-      if (tc_eligible(c)) {
-        const int64_t base = (int64_t)ch.size();
-        ch.resize((size_t)(base + chunk_floats_fwd(in_dim, H, K)));
-        chunk_layout_fwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
-          ch[(size_t)pos] = (uint32_t)(off + src) | (lo ? 0x80000000u : 0u);
-        });
-      }
-      if (H == 64) {
-        const int64_t base = (int64_t)bch.size();
-        bch.resize((size_t)(base + chunk_floats_bwd(in_dim, H, K)));
-        chunk_layout_bwd(in_dim, H, K, base, [&](int64_t pos, int64_t src, bool lo) {
-          bch[(size_t)pos] = (uint32_t)(off + src) | (lo ? 0x80000000u : 0u);
-        });
-      }
       off += mlp_param_count(in_dim, H, K);
     }
+  if (tc_eligible(c)) {
+    std::vector<int64_t> fo, bo;
+    int64_t nf = 0, nb = 0;
+    mp_chunk_plan(H, K, c->M, H == 64, [](bool, int64_t, int64_t, bool) {}, fo, bo, nf, nb);
+    ch.resize((size_t)nf);
+    bch.resize((size_t)nb);
+    mp_chunk_plan(
+        H, K, c->M, H == 64,
+        [&](bool fwd, int64_t pos, int64_t src, bool lo) {
+          (fwd ? ch : bch)[(size_t)pos] = (uint32_t)src | (lo ? 0x80000000u : 0u);
+        },
+        fo, bo, nf, nb);
+  }
   c->pt_src.upload(pt.data(), (int64_t)pt.size(), c->stream);
   c->ch_map.upload(ch.data(), (int64_t)ch.size(), c->stream);
   c->bch_map.upload(bch.data(), (int64_t)bch.size(), c->stream);

@@ -282,6 +282,16 @@ __device__ __forceinline__ uint64_t opaque64(uint64_t x) {
 
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
+// 3xTF32 high part: x rounded to the nearest tf32 (ties away from zero; two
+// integer ops). The residual x - hi is exact in fp32 and has a random sign
+// relative to x, so the tensor core's truncation of it to tf32 adds no
+// systematic bias (with a truncated hi the residual always has x's sign and
+// its truncation shrinks every product's magnitude by ~2^-21 — a bias that
+// survives sums over 10^5 rows).
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
 // fp32 -> tf32 (round to nearest, ties away), result kept in fp32 format.
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;

@@ -6,6 +6,8 @@ for E in ((int(sys.argv[1]),) if len(sys.argv) > 1 else (8,)):
     cfg = GnnConfig("p", H, M, k, mode="na2a")
     g = build_rank_graph(E, 5, 1, 0)
     eng = Engine(0); eng.upload_graph(g); eng.configure(cfg); eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+    if len(sys.argv) > 2:
+        eng.set_option("edge_factorized", int(sys.argv[2]))
     eng.synthetic_inputs(1)
     eng.step_device(); eng.step_device()
     eng.set_option("bwd_profile", 1)

