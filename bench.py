@@ -228,6 +228,8 @@ def main():
     ap.add_argument("--mode", default="na2a", choices=["na2a", "a2a", "none"],
                     help="halo exchange mode (configs[4] compares all three; none = the inconsistent baseline)")
     ap.add_argument("--halo-sm-reserve", type=int, default=-1, help="SMs left to the exchange (-1: engine default)")
+    ap.add_argument("--fact", type=int, default=-1, choices=[-1, 0, 1],
+                    help="edge_factorized option (-1: engine default)")
     ap.add_argument("--halo-overlap", type=int, default=1, choices=[0, 1],
                     help="1: forward exchange on a side stream, overlapped with the interior edges (N > 1)")
     a = ap.parse_args()
@@ -272,6 +274,8 @@ def main():
     eng.set_option("halo_overlap", a.halo_overlap)
     if a.halo_sm_reserve >= 0:
         eng.set_option("halo_sm_reserve", a.halo_sm_reserve)
+    if a.fact >= 0:
+        eng.set_option("edge_factorized", a.fact)
     eng.synthetic_inputs(seed=1234)
     stream = torch.cuda.ExternalStream(eng.stream_ptr)
 
@@ -311,6 +315,46 @@ def main():
         t = torch.tensor([float(g.num_local)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         sum_local = int(t.item())
+
+    # ---- halo time share (exposed and raw), N > 1 with an exchange.
+    # raw: pack + exchange + sync kernels of the serial schedule (compute
+    # stream, CUDA events) / serial step; exposed: extra step time of the
+    # default (overlapped) schedule over the same step without the exchange
+    # (mode none: the inconsistent baseline of configs[4]), both max over ranks.
+    halo = None
+    if world > 1 and wl["mode"] != "none" and not a.profile:
+        def timed_steps(k_steps):
+            barrier()
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0_.record(stream)
+            for _ in range(k_steps):
+                eng.step_device()
+            e1_.record(stream)
+            barrier()
+            t_ = torch.tensor([e0_.elapsed_time(e1_) / k_steps], dtype=torch.float64)
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            return float(t_.item())
+        k2 = max(2, a.steps // 2)
+        eng.set_option("halo_overlap", 0)
+        eng.step_device()
+        eng.kernel_timing(True)
+        t_serial = timed_steps(k2)
+        h_ms = eng.kernel_times()["halo"][0] / k2
+        eng.kernel_timing(False)
+        hm = torch.tensor([h_ms], dtype=torch.float64)
+        dist.all_reduce(hm, op=dist.ReduceOp.MAX)
+        eng.set_option("halo_overlap", a.halo_overlap)
+        eng.configure(GnnConfig("bench", H, M, k, mode="none"))
+        eng.step_device()
+        t_none = timed_steps(k2)
+        eng.configure(cfg)
+        halo = {"halo_raw_share": float(hm.item()) / t_serial, "halo_raw_ms_per_step": float(hm.item()),
+                "serial_ms_per_step": t_serial, "none_ms_per_step": t_none,
+                "halo_exposed_share": max(0.0, (ms_max - t_none) / ms_max),
+                "halo_exposed_ms_per_step": ms_max - t_none,
+                "basis": "raw = pack + exchange + sync kernels of the serial schedule (CUDA events, compute stream) "
+                         "/ serial step; exposed = (default-schedule step - same step with mode none) / "
+                         "default-schedule step; max over ranks"}
 
     # ---- roofline of the dominant kernel class (live CUDA-event durations)
     per_launch = {c: (t / max(nl_, 1), nl_) for c, (t, nl_) in ktimes.items()}
@@ -380,14 +424,10 @@ def main():
                 "config": config_dict(wl, n), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                 "cpu_baseline": cpu, "clocks": clk, "train_step": train, "hbm_kernels": hbm,
                 "kernel_share": {c: round(v, 4) for c, v in step_share.items()},
-                "halo_share": round(step_share.get("halo", 0.0), 4), "halo_bytes_per_step_rank0": halo_bytes,
+                "halo_bytes_per_step_rank0": halo_bytes,
                 "halo_overlap": bool(a.halo_overlap and n > 1 and wl["mode"] != "none"),
                 "halo_sm_reserve": a.halo_sm_reserve,
-                "halo_share_basis": ("forward: pack + NCCL on a side stream overlapped with the interior edges "
-                                     "(time not exposed); backward: adjoint exchange + sync on the compute stream"
-                                     if a.halo_overlap and n > 1 else
-                                     "raw = exposed: pack + NCCL send/recv + sync run on the compute stream "
-                                     "between aggregation and node update (no overlap)"),
+                **(halo or {}),
                 "sum_local_rows": sum_local,
                 "harness_layer_rows_per_s": sum_local * M / (ms_max / 1e3),
                 "graph_build_s": round(t_graph, 3),

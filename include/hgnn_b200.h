@@ -188,7 +188,7 @@ int hgnn_get_grads(hgnn_ctx* ctx, double* mp_grads);
 /* Model level: node / edge encoders and the decoder on  */
 /* the device around the MP stack, the consistent loss, rank-averaged          */
 /* gradients and Adam — compute_gradients / train_step (model.cpp:556-579).   */
-/* Hidden width 64, feature widths (F_x, F_e, F_y) = (3, 7, 3).               */
+/* Hidden width 32 or 64, feature widths (F_x, F_e, F_y) = (3, 7, 3).        */
 /* ========================================================================== */
 /* After hgnn_configure: feature widths (GnnConfig in_node_dim, in_edge_dim, out_dim). */
 int hgnn_model_configure(hgnn_ctx* ctx, int64_t in_node_dim, int64_t in_edge_dim, int64_t out_dim);

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhgnn_b200.so"
+# HGNN_B200_LIB: alternative build of the same library (timing experiments, scripts/build_exp.py)
+_LIB_PATH = Path(os.environ.get("HGNN_B200_LIB") or Path(__file__).resolve().parent / "lib" / "libhgnn_b200.so")
 
 
 class Error(RuntimeError):

@@ -26,143 +26,187 @@
 namespace hgnn_b200 {
 
 constexpr int kFactThreads = 256;
+constexpr int kFactRows = 64;  // nodes per block iteration
 
 // P[i] = x_i [W0_s | W0_d] for local rows i < n. W0 rows 0..2H-1 (in x H,
-// row-major) are exactly [W0_s; W0_d].
+// row-major) are exactly [W0_s; W0_d]: P = X W with W = [W0_s | W0_d] (H x 2H).
+// Register-blocked: warp w owns nodes 8 w .. 8 w + 7 of the 64-node tile, lane
+// l outputs 4 l .. 4 l + 3; per k one broadcast pair of 16-byte loads (8 x
+// values, from the transposed tile) and one 16-byte weight load feed 32 FMAs.
 template <int H>
 __global__ void __launch_bounds__(kFactThreads) edge_proj_kernel(const float* __restrict__ x,
                                                                  const float* __restrict__ w0, int64_t n,
                                                                  float* __restrict__ P) {
-  constexpr int TPN = 2 * H / 8;                // threads per node (8 outputs each)
-  constexpr int NPB = kFactThreads / TPN;       // nodes per block iteration
-  __shared__ __align__(16) float ws[2 * H * H];  // [k'][j], k' < 2H: W0_s rows then W0_d rows
-  __shared__ __align__(16) float xs[NPB][H];
-  for (int i = threadIdx.x; i < 2 * H * H / 4; i += blockDim.x)
-    reinterpret_cast<float4*>(ws)[i] = __ldg(reinterpret_cast<const float4*>(w0) + i);
-  const int nl = threadIdx.x / TPN, o = threadIdx.x % TPN;
-  const int half = (8 * o) / H, j0 = (8 * o) % H;  // output block: P_s or P_d, columns j0..j0+7
-  for (int64_t base = (int64_t)blockIdx.x * NPB; base < n; base += (int64_t)gridDim.x * NPB) {
+  static_assert(H == 64, "the factorised edge path is built for H = 64");
+  constexpr int NO = 2 * H;              // outputs per node (= 4 x 32 lanes)
+  constexpr int XS = kFactRows + 4;      // transposed tile row stride
+  extern __shared__ __align__(16) float fsm[];
+  float* ws = fsm;                       // [k][NO]: W[k][o] = (o < H ? W0_s[k][o] : W0_d[k][o - H])
+  float* xt = fsm + H * NO;              // [k][XS]: x transposed
+  for (int t = threadIdx.x; t < H * NO; t += blockDim.x) {
+    const int k = t / NO, o = t % NO;
+    ws[t] = __ldg(w0 + (int64_t)((o < H ? 0 : H) + k) * H + (o % H));
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int64_t base = (int64_t)blockIdx.x * kFactRows; base < n; base += (int64_t)gridDim.x * kFactRows) {
     __syncthreads();
-    for (int t = threadIdx.x; t < NPB * H / 4; t += blockDim.x) {
-      const int r = t / (H / 4), c = t % (H / 4);
-      const int64_t i = base + r;
-      reinterpret_cast<float4*>(&xs[r][0])[c] =
-          i < n ? __ldg(reinterpret_cast<const float4*>(x + i * H) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // lanes walk rows (conflict-free transposed stores); the other column
+    // pieces of each row are read by the neighbouring warps from L1
+    for (int t = threadIdx.x; t < kFactRows * H / 4; t += blockDim.x) {
+      const int r = t % kFactRows, c = t / kFactRows;
+      const float4 v = base + r < n ? __ldg(reinterpret_cast<const float4*>(x + (base + r) * H) + c)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      xt[(4 * c) * XS + r] = v.x;
+      xt[(4 * c + 1) * XS + r] = v.y;
+      xt[(4 * c + 2) * XS + r] = v.z;
+      xt[(4 * c + 3) * XS + r] = v.w;
     }
     __syncthreads();
-    float acc[8];
+    float acc[8][4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[a][q] = 0.f;
 #pragma unroll 4
     for (int k = 0; k < H; ++k) {
-      const float xv = xs[nl][k];
-      const float4 wa = *reinterpret_cast<const float4*>(&ws[(half * H + k) * H + j0]);
-      const float4 wb = *reinterpret_cast<const float4*>(&ws[(half * H + k) * H + j0 + 4]);
-      acc[0] = fmaf(xv, wa.x, acc[0]);
-      acc[1] = fmaf(xv, wa.y, acc[1]);
-      acc[2] = fmaf(xv, wa.z, acc[2]);
-      acc[3] = fmaf(xv, wa.w, acc[3]);
-      acc[4] = fmaf(xv, wb.x, acc[4]);
-      acc[5] = fmaf(xv, wb.y, acc[5]);
-      acc[6] = fmaf(xv, wb.z, acc[6]);
-      acc[7] = fmaf(xv, wb.w, acc[7]);
+      const float4 x0 = *reinterpret_cast<const float4*>(xt + k * XS + 8 * warp);
+      const float4 x1 = *reinterpret_cast<const float4*>(xt + k * XS + 8 * warp + 4);
+      const float xa[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      const float4 wv = *reinterpret_cast<const float4*>(ws + k * NO + 4 * lane);
+      const float w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(xa[a], w[q], acc[a][q]);
     }
-    const int64_t i = base + nl;
-    if (i < n) {
-      float4* out = reinterpret_cast<float4*>(P + i * 2 * H + half * H + j0);
-      out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int64_t i = base + 8 * warp + a;
+      if (i < n)
+        *reinterpret_cast<float4*>(P + i * NO + 4 * lane) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
     }
   }
 }
+template <int H>
+constexpr size_t edge_proj_smem() { return (size_t)(H * 2 * H + H * (kFactRows + 4)) * 4; }
 
-// Backward of the node-level input projection, rows [0, rows):
-//   dx_i = (i < n_local ? dx_node_i : 0) + S_src W0_s^T + S_dst W0_d^T
-// and per-block partials of dW0_s / dW0_d: part[block][0 .. H*H) = dW0_s,
-// [H*H .. 2*H*H) = dW0_d (row-major k x j, the layout of W0's row blocks).
+// Backward of the node-level input projection, rows [0, rows), 64 per block
+// iteration:
+//   S = [S_src | S_dst] (segment sums of dY through the twin / slot index)
+//   dx_i = (i < n_local ? dx_node_i : 0) + S_i [W0_s^T ; W0_d^T]
+//   dW[k][j] += sum_i x_i[k] S_i[j]  (j < H: dW0_s, j >= H: dW0_d)
+// per-block partials part[block][k * 2H + j] (fixed ownership, nodes in
+// order): reduced in block order by grad_reduce_add_kernel after a reorder
+// into W0's row layout (k x H blocks).
 template <int H>
 __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
     const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ dx_node,
     const float* __restrict__ w0, const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
     const int32_t* __restrict__ twin, int64_t rows, int64_t n_local, float* __restrict__ dx,
     float* __restrict__ part) {
-  constexpr int NC = kFactThreads / (H / 4);  // nodes per chunk (one float4 column group per thread)
-  constexpr int OUT4 = H / 4;                 // dx: threads per node in the product phase = H / 4 (4 outputs each)
-  constexpr int NW = 2 * H * H / kFactThreads;  // dW elements per thread (split between s and d)
-  __shared__ __align__(16) float wt[2][H][H];   // wt[s][j][k] = W0_s[k][j] (s = 0) / W0_d[k][j] (s = 1)
-  __shared__ __align__(16) float ss[2][NC][H];  // S_src, S_dst of the chunk's nodes
-  __shared__ __align__(16) float xs[NC][H];
-  for (int t = threadIdx.x; t < 2 * H * H; t += blockDim.x) {
-    const int s = t / (H * H), k = (t / H) % H, j = t % H;  // coalesced read of W0 row block s
-    wt[s][j][k] = __ldg(w0 + t);
+  static_assert(H == 64, "the factorised edge path is built for H = 64");
+  constexpr int NS = 2 * H;  // S width
+  constexpr int WK = 4;      // dW: thread owns 4 k-rows x 8 j-columns (16 x 16 thread grid)
+  constexpr int WJ = 8;
+  extern __shared__ __align__(16) float fsm[];
+  float* wt = fsm;                  // [j][o] (j < 2H, o < H): W0_s[o][j] (j < H), W0_d[o][j - H]
+  float* sr = wt + NS * H;          // [r][NS]: S rows
+  float* xr = sr + kFactRows * NS;  // [r][H]: x rows
+  for (int t = threadIdx.x; t < NS * H; t += blockDim.x) {
+    const int j = t / H, o = t % H;
+    wt[t] = __ldg(w0 + (int64_t)((j < H ? 0 : H) + o) * H + (j % H));
   }
-  // dW ownership: thread owns (s, k, j0 .. j0 + NW/2) of both blocks? -> element e = threadIdx.x * NW / 2 + q of
-  // each block (row-major k x j): NW / 2 consecutive elements per block.
-  constexpr int PER = NW / 2;
-  const int e0 = threadIdx.x * PER;
-  const int wk = e0 / H, wj0 = e0 % H;
-  float acc_s[PER], acc_d[PER];
+  const int g16 = threadIdx.x / 16, l16 = threadIdx.x % 16;
+  float accw[WK][WJ];
 #pragma unroll
-  for (int q = 0; q < PER; ++q) acc_s[q] = acc_d[q] = 0.f;
-  const int nd = threadIdx.x / OUT4, oc = threadIdx.x % OUT4;  // gather / product phase mapping
-  for (int64_t base = (int64_t)blockIdx.x * NC; base < rows; base += (int64_t)gridDim.x * NC) {
+  for (int a = 0; a < WK; ++a)
+#pragma unroll
+    for (int b = 0; b < WJ; ++b) accw[a][b] = 0.f;
+  for (int64_t base = (int64_t)blockIdx.x * kFactRows; base < rows; base += (int64_t)gridDim.x * kFactRows) {
     __syncthreads();
-    {  // segment sums, one float4 column group per thread
-      const int64_t i = base + nd;
-      float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s1, xv = s1;
+    // segment sums, item (r, c4): lanes 0-15 of a warp read the twin row
+    // (S_src), lanes 16-31 the slot row (S_dst): 256-byte coalesced pieces
+    for (int t = threadIdx.x; t < kFactRows * NS / 4; t += blockDim.x) {
+      const int r = t / (NS / 4), c4 = t % (NS / 4);
+      const bool src_half = c4 < H / 4;
+      const int cc = src_half ? c4 : c4 - H / 4;
+      const int64_t i = base + r;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
       if (i < rows) {
         const int32_t p1 = __ldg(end + i);
         for (int32_t p = __ldg(beg + i); p < p1; ++p) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(dy + (int64_t)__ldg(twin + p) * H) + oc);
-          const float4 b = __ldg(reinterpret_cast<const float4*>(dy + (int64_t)p * H) + oc);
-          s1 = make_float4(s1.x + a.x, s1.y + a.y, s1.z + a.z, s1.w + a.w);
-          s2 = make_float4(s2.x + b.x, s2.y + b.y, s2.z + b.z, s2.w + b.w);
+          const int64_t e = src_half ? (int64_t)__ldg(twin + p) : (int64_t)p;
+          const float4 v = __ldg(reinterpret_cast<const float4*>(dy + e * H) + cc);
+          s = make_float4(s.x + v.x, s.y + v.y, s.z + v.z, s.w + v.w);
         }
-        if (i < n_local) xv = __ldg(reinterpret_cast<const float4*>(x + i * H) + oc);
       }
-      reinterpret_cast<float4*>(&ss[0][nd][0])[oc] = s1;
-      reinterpret_cast<float4*>(&ss[1][nd][0])[oc] = s2;
-      reinterpret_cast<float4*>(&xs[nd][0])[oc] = xv;
+      *reinterpret_cast<float4*>(sr + r * NS + 4 * c4) = s;
+    }
+    for (int t = threadIdx.x; t < kFactRows * H / 4; t += blockDim.x) {
+      const int r = t / (H / 4), c = t % (H / 4);
+      const int64_t i = base + r;
+      *reinterpret_cast<float4*>(xr + r * H + 4 * c) =
+          i < n_local ? __ldg(reinterpret_cast<const float4*>(x + i * H) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
-    {  // dx = dx_node + S_src W0_s^T + S_dst W0_d^T, 4 outputs per thread
-      const int64_t i = base + nd;
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    {  // dx: thread = nodes 4 g16 .. +3 x outputs 4 l16 .. +3
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[a][q] = 0.f;
 #pragma unroll 4
-      for (int j = 0; j < H; ++j) {
-        const float a = ss[0][nd][j], b = ss[1][nd][j];
-        const float4 u = *reinterpret_cast<const float4*>(&wt[0][j][4 * oc]);
-        const float4 v = *reinterpret_cast<const float4*>(&wt[1][j][4 * oc]);
-        o.x = fmaf(a, u.x, fmaf(b, v.x, o.x));
-        o.y = fmaf(a, u.y, fmaf(b, v.y, o.y));
-        o.z = fmaf(a, u.z, fmaf(b, v.z, o.z));
-        o.w = fmaf(a, u.w, fmaf(b, v.w, o.w));
+      for (int j = 0; j < NS; ++j) {
+        float sa[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) sa[a] = sr[(4 * g16 + a) * NS + j];
+        const float4 wv = *reinterpret_cast<const float4*>(wt + j * H + 4 * l16);
+        const float w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[a][q] = fmaf(sa[a], w[q], acc[a][q]);
       }
-      if (i < rows) {
-        if (i < n_local) {
-          const float4 d = __ldg(reinterpret_cast<const float4*>(dx_node + i * H) + oc);
-          o = make_float4(o.x + d.x, o.y + d.y, o.z + d.z, o.w + d.w);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t i = base + 4 * g16 + a;
+        if (i < rows) {
+          float4 o = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+          if (i < n_local) {
+            const float4 d = __ldg(reinterpret_cast<const float4*>(dx_node + i * H) + l16);
+            o = make_float4(o.x + d.x, o.y + d.y, o.z + d.z, o.w + d.w);
+          }
+          reinterpret_cast<float4*>(dx + i * H)[l16] = o;
         }
-        reinterpret_cast<float4*>(dx + i * H)[oc] = o;
       }
     }
-    // dW0_s[k][j] += x[k] S_src[j], dW0_d[k][j] += x[k] S_dst[j], nodes in order
+    // dW: thread owns k in [4 g16, +4), j in [8 l16, +8); nodes in order
 #pragma unroll 2
-    for (int n = 0; n < NC; ++n) {
-      const float xk = xs[n][wk];
+    for (int r = 0; r < kFactRows; ++r) {
+      const float4 xv = *reinterpret_cast<const float4*>(xr + r * H + WK * g16);
+      const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+      const float4 s0 = *reinterpret_cast<const float4*>(sr + r * NS + WJ * l16);
+      const float4 s1 = *reinterpret_cast<const float4*>(sr + r * NS + WJ * l16 + 4);
+      const float sb[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        acc_s[q] = fmaf(xk, ss[0][n][wj0 + q], acc_s[q]);
-        acc_d[q] = fmaf(xk, ss[1][n][wj0 + q], acc_d[q]);
-      }
+      for (int a = 0; a < WK; ++a)
+#pragma unroll
+        for (int b = 0; b < WJ; ++b) accw[a][b] = fmaf(xa[a], sb[b], accw[a][b]);
     }
   }
+  // partial in W0's layout: rows 0..H-1 = W0_s (j < H), rows H..2H-1 = W0_d
   float* ps = part + (int64_t)blockIdx.x * 2 * H * H;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    ps[e0 + q] = acc_s[q];
-    ps[H * H + e0 + q] = acc_d[q];
-  }
+  for (int a = 0; a < WK; ++a)
+#pragma unroll
+    for (int b = 0; b < WJ; ++b) {
+      const int k = WK * g16 + a, j = WJ * l16 + b;
+      ps[(j < H ? 0 : H * H) + k * H + (j % H)] = accw[a][b];
+    }
+}
+template <int H>
+constexpr size_t edge_input_adjoint_smem() {
+  return (size_t)(2 * H * H + kFactRows * 2 * H + kFactRows * H) * 4;
 }
 
 // out[i] += sum_b part[b][i] in block order (fp64): the node-level W0_s / W0_d

@@ -13,7 +13,9 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "edge_fact.cuh"
@@ -35,9 +37,62 @@ void bind(hgnn_ctx* c) {
 }
 
 
+// Waits for the stream with a deadline; on expiry aborts the communicator so
+// the stuck NCCL kernels end, and raises CollectiveError (instead of hanging).
+void nccl_wait_or_abort(hgnn_ctx* c, cudaStream_t st, const char* what) {
+  cudaEvent_t ev;
+  CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_OK(cudaEventRecord(ev, st));
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaError_t q;
+  while ((q = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(c->coll_timeout_ms)) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      c->comm_aborted = true;
+      cudaEventDestroy(ev);
+      fail(HGNN_ERR_COLLECTIVE, std::string("collective aborted: ") + what + " did not complete within " +
+                                    std::to_string(c->coll_timeout_ms) + " ms (a rank is missing or out of sequence)");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  cudaEventDestroy(ev);
+  if (q != cudaSuccess) CUDA_OK(q);
+}
+
+// Debug guard (option "collective_check"): before every collective each rank
+// all-gathers (kind, mode, count, sequence number); any difference raises
+// CollectiveError on every rank — the reference's poisoning of mismatched
+// collective sequences (comm.cpp:184-188) — and a rank that never arrives
+// times out into ncclCommAbort.
+void nccl_check_sequence(hgnn_ctx* c, int kind, int64_t count) {
+  if (!c->coll_check || !c->comm) {
+    if (c->comm_aborted) fail(HGNN_ERR_COLLECTIVE, "collective aborted: the communicator was aborted");
+    return;
+  }
+  const int R = c->nranks;
+  c->coll_sig.alloc(4 * (int64_t)(R + 1));
+  const int32_t mine[4] = {kind, c->mode, (int32_t)count, (int32_t)c->coll_seq++};
+  CUDA_OK(cudaMemcpyAsync(c->coll_sig.p, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+  NCCL_OK(ncclAllGather(c->coll_sig.p, c->coll_sig.p + 4, 4, ncclInt32, c->comm, c->stream));
+  nccl_wait_or_abort(c, c->stream, "collective sequence check");
+  std::vector<int32_t> all((size_t)(4 * R));
+  CUDA_OK(cudaMemcpy(all.data(), c->coll_sig.p + 4, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost));
+  for (int r = 0; r < R; ++r)
+    for (int q = 0; q < 4; ++q)
+      if (all[(size_t)(4 * r + q)] != all[(size_t)q])
+        fail(HGNN_ERR_COLLECTIVE, "collective aborted: mismatched collective sequence (rank " + std::to_string(r) +
+                                      " posted kind " + std::to_string(all[(size_t)(4 * r)]) + " mode " +
+                                      std::to_string(all[(size_t)(4 * r + 1)]) + " #" +
+                                      std::to_string(all[(size_t)(4 * r + 3)]) + ", rank 0 kind " +
+                                      std::to_string(all[0]) + " mode " + std::to_string(all[1]) + " #" +
+                                      std::to_string(all[3]) + ")");
+}
+
 void allreduce_sum_f64(hgnn_ctx* c, double* d, int64_t n) {
   if (c->nranks <= 1 || n <= 0) return;
-  if (c->comm) {
+  if (c->comm || c->comm_aborted) {
+    nccl_check_sequence(c, kCollAllReduce, n);
     NCCL_OK(ncclAllReduce(d, d, (size_t)n, ncclDouble, ncclSum, c->comm, c->stream));
   } else if (c->group) {
     std::vector<double> h((size_t)n);
@@ -184,12 +239,13 @@ void ensure_buffers(hgnn_ctx* c) {
     c->ps.clear();
     for (int64_t m = 0; m < M; ++m) {
       c->ps.emplace_back(new DevBuf<float>());
-      if (c->edge_fact && c->fact_ok && tc_eligible(c)) c->ps.back()->alloc(c->rows * 2 * H);
+      if (c->edge_fact && c->fact_ok && H == 64) c->ps.back()->alloc(c->rows * 2 * H);
     }
   }
   if (c->ps_ready.size() != (size_t)M) c->ps_ready.assign((size_t)M, 0);
-  c->fact_blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (c->rows + 15) / 16), (int64_t)c->num_sms * 4);
-  if (c->edge_fact && c->fact_ok && tc_eligible(c)) c->fact_part.alloc((int64_t)c->fact_blocks * 2 * H * H);
+  c->fact_blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (c->rows + kFactRows - 1) / kFactRows),
+                                          (int64_t)c->num_sms * 2);
+  if (c->edge_fact && c->fact_ok && H == 64) c->fact_part.alloc((int64_t)c->fact_blocks * 2 * H * H);
   c->stage_elems = std::min<int64_t>(std::max<int64_t>(c->rows, c->ne) * H, int64_t{1} << 24);
   c->stage.alloc(std::max<int64_t>(c->stage_elems, 1));
   // halo buffers
@@ -376,11 +432,13 @@ void local_halo_exchange_adjoint(hgnn_ctx* c, float* d_a, cudaStream_t st) {
 }
 
 void halo_exchange(hgnn_ctx* c, float* a, cudaStream_t st) {
-  Timed t(c, HGNN_K_HALO, st);
   if (c->group) {
+    Timed t(c, HGNN_K_HALO, st);
     local_halo_exchange(c, a, st);
     return;
   }
+  if (c->nranks > 1) nccl_check_sequence(c, kCollHaloFwd, c->H);
+  Timed t(c, HGNN_K_HALO, st);
   const int64_t H = c->H;
   const int R = c->nranks;
   if (c->mode == HGNN_MODE_NA2A) {
@@ -426,6 +484,7 @@ void halo_exchange(hgnn_ctx* c, float* a, cudaStream_t st) {
 }
 
 void halo_exchange_adjoint(hgnn_ctx* c, float* d_a, cudaStream_t st) {
+  if (!c->group && c->nranks > 1 && c->mode != HGNN_MODE_NONE) nccl_check_sequence(c, kCollHaloAdj, c->H);
   Timed t(c, HGNN_K_HALO, st);
   const int64_t H = c->H;
   const int R = c->nranks;
@@ -533,49 +592,60 @@ void launch_tc_forward(hgnn_ctx* c, int mode, int64_t m, int64_t n_rows, const f
   }
 }
 
-bool use_fact(const hgnn_ctx* c) { return c->edge_fact && c->fact_ok && tc_eligible(c); }
-bool use_fact_fwd(const hgnn_ctx* c) { return use_tc(c) && use_fact(c); }
+bool use_fact(const hgnn_ctx* c) { return c->edge_fact && c->fact_ok && c->H == 64; }
+bool use_fused_fwd(const hgnn_ctx* c) { return use_tc(c) && c->fact_ok; }
 
 // P_m = x_m [W0_s | W0_d] on the local rows (edges never reference halo rows)
 void edge_proj(hgnn_ctx* c, int64_t m, const float* x) {
   Timed t(c, HGNN_K_EDGE_PROJ);
   if (c->nl == 0) return;
   const float* w0 = layer_params(c, m, true).p;
-  const unsigned grid = (unsigned)std::min<int64_t>((c->nl + 15) / 16, (int64_t)c->num_sms * 8);
-  if (c->H == 64) edge_proj_kernel<64><<<grid, kFactThreads, 0, c->stream>>>(x, w0, c->nl, c->ps[(size_t)m]->p);
-  else edge_proj_kernel<32><<<grid, kFactThreads, 0, c->stream>>>(x, w0, c->nl, c->ps[(size_t)m]->p);
+  constexpr size_t smem = edge_proj_smem<64>();
+  CUDA_OK(cudaFuncSetAttribute(edge_proj_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)std::min<int64_t>((c->nl + kFactRows - 1) / kFactRows, (int64_t)c->num_sms * 4);
+  edge_proj_kernel<64><<<grid, kFactThreads, smem, c->stream>>>(x, w0, c->nl, c->ps[(size_t)m]->p);
   check_launch(c);
   c->ps_ready[(size_t)m] = 1;
 }
 
 // The fused edge update (kEdgeFact): tiles [t0, t1) of the segment table;
 // writes e' (es[m + 1]) and the aggregate of every receiver in those tiles.
-template <int H>
-void launch_fact_typed(hgnn_ctx* c, const TcFwdArgs& args) {
-  auto k = mlp_tc_forward_kernel<H, kEdgeFact, false>;
+template <int H, int MODE>
+void launch_fused_typed(hgnn_ctx* c, const TcFwdArgs& args) {
+  auto k = mlp_tc_forward_kernel<H, MODE, false>;
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<H>::SMEM_FACT));
   const int64_t pairs = (args.n_tiles + 1) / 2;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms - c->sm_reserve));
   k<<<grid, TcCfg<H>::THREADS, TcCfg<H>::SMEM_FACT, c->stream>>>(args);
   check_launch(c);
 }
-void launch_fact_forward(hgnn_ctx* c, int64_t m, int64_t t0, int64_t t1, const float* e, float* e2, float* a) {
+// The fused edge update: tiles [t0, t1) of the receiver-segment table; writes
+// e' (e2) and the aggregate of every receiver in those tiles. kEdgeFact when
+// the input linear is factorised through the nodes, else kEdgeFused.
+void launch_fused_forward(hgnn_ctx* c, int64_t m, int64_t t0, int64_t t1, const float* x, const float* e, float* e2,
+                          float* a) {
   if (t1 <= t0) return;
+  const bool fact = use_fact(c);
   TcFwdArgs args{};
   args.n_tiles = t1 - t0;
   args.tiles = c->tiles.p + t0;
   args.src = c->src.p;
   args.dst = c->dst.p;
   args.inv = c->inv.p;
+  args.x = x;
   args.e_in = e;
   args.out = e2;
   args.agg = a;
-  args.proj = c->ps[(size_t)m]->p;
-  args.chunks = c->chunks.p + c->chunk_off[(size_t)(3 * m + 2)];
+  args.proj = fact ? c->ps[(size_t)m]->p : nullptr;
+  args.chunks = c->chunks.p + c->chunk_off[(size_t)(3 * m + (fact ? 2 : 0))];
   args.params = layer_params(c, m, true).p;
   args.k = (int)c->K;
-  if (c->H == 64) launch_fact_typed<64>(c, args);
-  else launch_fact_typed<32>(c, args);
+  if (c->H == 64) {
+    if (fact) launch_fused_typed<64, kEdgeFact>(c, args);
+    else launch_fused_typed<64, kEdgeFused>(c, args);
+  } else {
+    launch_fused_typed<32, kEdgeFused>(c, args);
+  }
 }
 void zero_empty_rows(hgnn_ctx* c, float* a) {
   if (c->n_rows_empty == 0) return;
@@ -643,17 +713,17 @@ bool can_overlap(const hgnn_ctx* c) {
   return c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group);
 }
 
-// Edge update of the factorised MP layer: node projections, then ONE fused
-// kernel (gather -> tcgen05 MLP -> e' + segmented 1/d aggregate); with an
-// exchange, the boundary tiles first and the exchange on the side stream
-// while the interior tiles run.
-void layer_forward_fact(hgnn_ctx* c, int64_t m, float* x, float* e, float* e2, float* a, float* x2) {
-  edge_proj(c, m, x);
+// Edge update as ONE fused kernel (gather -> tcgen05 MLP -> e' + segmented
+// 1/d aggregate), after the node projections when the input linear is
+// factorised; with an exchange, the boundary tiles first and the exchange on
+// the side stream while the interior tiles run.
+void layer_forward_fused(hgnn_ctx* c, int64_t m, float* x, float* e, float* e2, float* a, float* x2) {
+  if (use_fact(c)) edge_proj(c, m, x);
   zero_empty_rows(c, a);  // empty segments (halo rows: before the receive overwrites them)
   if (can_overlap(c) && c->n_tiles_bnd > 0) {
     {
       Timed t(c, HGNN_K_EDGE_FWD);
-      launch_fact_forward(c, m, 0, c->n_tiles_bnd, e, e2, a);
+      launch_fused_forward(c, m, 0, c->n_tiles_bnd, x, e, e2, a);
     }
     CUDA_OK(cudaEventRecord(c->ev_bnd, c->stream));
     CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_bnd, 0));
@@ -662,7 +732,7 @@ void layer_forward_fact(hgnn_ctx* c, int64_t m, float* x, float* e, float* e2, f
     {
       Timed t(c, HGNN_K_EDGE_FWD);
       c->sm_reserve = c->halo_sm_reserve;
-      launch_fact_forward(c, m, c->n_tiles_bnd, c->n_tiles, e, e2, a);
+      launch_fused_forward(c, m, c->n_tiles_bnd, c->n_tiles, x, e, e2, a);
       c->sm_reserve = 0;
     }
     CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
@@ -670,7 +740,7 @@ void layer_forward_fact(hgnn_ctx* c, int64_t m, float* x, float* e, float* e2, f
   } else {
     {
       Timed t(c, HGNN_K_EDGE_FWD);
-      launch_fact_forward(c, m, 0, c->n_tiles, e, e2, a);
+      launch_fused_forward(c, m, 0, c->n_tiles, x, e, e2, a);
     }
     if (c->mode != HGNN_MODE_NONE) {
       halo_exchange(c, a, c->stream);
@@ -687,8 +757,8 @@ void layer_forward(hgnn_ctx* c, int64_t m) {
   float* e2 = c->es[m + 1]->p;
   float* a = c->as[m]->p;
   float* x2 = c->xs[m + 1]->p;
-  if (use_fact_fwd(c)) {
-    layer_forward_fact(c, m, x, e, e2, a, x2);
+  if (use_fused_fwd(c)) {
+    layer_forward_fused(c, m, x, e, e2, a, x2);
     return;
   }
   if (c->halo_overlap && c->mode != HGNN_MODE_NONE && c->nranks > 1 && (c->comm || c->group) && c->n_rows_bnd > 0 &&
@@ -927,12 +997,11 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
   if (fact) {  // input-node adjoint through the node-level sums of dY (edge_fact.cuh), + dW0_s / dW0_d
     Timed t(c, HGNN_K_DX);
     const float* w0 = layer_params(c, m, true).p;
-    if (H == 64)
-      edge_input_adjoint_kernel<64><<<c->fact_blocks, kFactThreads, 0, c->stream>>>(
-          c->dsrc.p, x, c->dxn.p, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
-    else
-      edge_input_adjoint_kernel<32><<<c->fact_blocks, kFactThreads, 0, c->stream>>>(
-          c->dsrc.p, x, c->dxn.p, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
+    constexpr size_t smem = edge_input_adjoint_smem<64>();
+    CUDA_OK(cudaFuncSetAttribute(edge_input_adjoint_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    edge_input_adjoint_kernel<64><<<c->fact_blocks, kFactThreads, smem, c->stream>>>(
+        c->dsrc.p, x, c->dxn.p, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
     check_launch(c);
     const int64_t nw = 2 * H * H;  // W0 rows 0 .. 2H-1 (x_src, x_dst blocks) of the edge MLP
     grad_reduce_add_kernel<<<blocks_for(nw), kEwThreads, 0, c->stream>>>(c->fact_part.p, c->fact_blocks, nw,
@@ -1509,6 +1578,13 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "edge_factorized: 0 (3-segment edge kernels) or 1");
       if (c->edge_fact != (int)value) c->ps.clear();  // (re)allocated by ensure_buffers
       c->edge_fact = (int)value;
+    } else if (k == "collective_check") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "collective_check: 0 or 1");
+      c->coll_check = (int)value;
+    } else if (k == "collective_timeout_ms") {
+      if (value <= 0) fail(HGNN_ERR_CONFIG, "collective_timeout_ms must be positive");
+      c->coll_timeout_ms = value;
+      if (c->group) c->group->timeout_ms = value;
     } else if (k == "mlp_backward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
       c->bwd_impl = (int)value;

@@ -67,6 +67,13 @@ struct hgnn_ctx {
   int32_t rank = 0, nranks = 1;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  // debug collective-sequence guard for the NCCL path (option "collective_check",
+  // the reference poisons mismatched sequences, comm.cpp:168-208)
+  int coll_check = 0;
+  int64_t coll_timeout_ms = 120000;
+  int64_t coll_seq = 0;
+  bool comm_aborted = false;
+  hgnn_b200::DevBuf<int32_t> coll_sig;
   // in-process rank group (hgnn_ctx_create_local): the exchange and the
   // all-reduces rendezvous on the host and copy device-to-device
   hgnn_b200::LocalGroup* group = nullptr;
@@ -120,7 +127,7 @@ struct hgnn_ctx {
   // factorised edge MLP (kEdgeFact, edge_fact.cuh): receiver-segment tiles of
   // the fused edge kernel ([0, n_tiles_bnd) cover the boundary slots), rows
   // with an empty segment (zeroed aggregate), node projections per layer
-  int edge_fact = 1;              // option "edge_factorized"
+  int edge_fact = 0;              // option "edge_factorized"
   bool fact_ok = false;           // every receiver segment fits one 128-slot tile
   hgnn_b200::DevBuf<int32_t> tiles, rows_empty;
   int64_t n_tiles = 0, n_tiles_bnd = 0, n_rows_empty = 0;

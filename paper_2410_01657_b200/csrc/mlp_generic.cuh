@@ -1,7 +1,7 @@
 // Encoder / decoder MLPs (SIMT fp32, sm_100a): the row-wise MLPs on either
 // side of the message-passing stack.
 //
-// Spec (nn.hpp:27-58, model.cpp:70-101), H = 64 hidden width, k hidden blocks:
+// Spec (nn.hpp:27-58, model.cpp:70-101), H = 32 or 64 hidden width, k hidden blocks:
 //   h = x W0 + b0;  h += ELU(LN0(h Wj + bj)), j = 1..k;
 //   y = h W_{k+1} + b_{k+1} (+ x W_skip);  y = LN(y) * gamma + beta (encoders)
 // encoder: IN = F_x or F_e, OUT = H, skip + output LayerNorm (model.cpp:70-80)
@@ -26,24 +26,20 @@
 namespace hgnn_b200 {
 
 constexpr int kGenThreads = 128;
-constexpr int kGenH = 64;
 constexpr int kGenRow = 68;  // staged row stride (floats): 16-byte aligned, conflict-free float4 row writes
 
-__host__ __device__ inline int64_t gen_param_count(int in_dim, int out_dim, int k, bool skip, bool out_ln) {
-  const int H = kGenH;
+__host__ __device__ inline int64_t gen_param_count(int in_dim, int out_dim, int k, bool skip, bool out_ln, int H) {
   return (int64_t)in_dim * H + H + (int64_t)k * (H * H + H) + (int64_t)H * out_dim + out_dim +
          (skip ? (int64_t)in_dim * out_dim : 0) + (out_ln ? 2 * out_dim : 0);
 }
 
 // Offsets (floats) inside one MLP's for_each block.
 struct GenLayout {
-  int in_dim, out_dim, k;
+  int in_dim, out_dim, k, H;
   __host__ __device__ int64_t w(int l) const {  // l = 0 .. k+1
-    const int H = kGenH;
     return l == 0 ? 0 : (int64_t)in_dim * H + H + (int64_t)(l - 1) * (H * H + H);
   }
   __host__ __device__ int64_t b(int l) const {
-    const int H = kGenH;
     return w(l) + (l == 0 ? (int64_t)in_dim * H : (l <= k ? (int64_t)H * H : (int64_t)H * out_dim));
   }
   __host__ __device__ int64_t skip() const { return b(k + 1) + out_dim; }
@@ -179,12 +175,11 @@ __device__ __forceinline__ void gen_stage_params(float* dst, const float* __rest
 }
 
 // ------------------------------------------------------------------ forward
-template <int IN, int OUT, bool SKIP, bool OUT_LN>
+template <int IN, int OUT, bool SKIP, bool OUT_LN, int H>
 __global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a) {
-  constexpr int H = kGenH;
   extern __shared__ __align__(16) float gsm[];
-  const GenLayout L{IN, OUT, a.k};
-  float* col = gsm + ((a.n_par + 3) / 4) * 4 + threadIdx.x;  // this thread's column (kGenH x kGenThreads)
+  const GenLayout L{IN, OUT, a.k, H};
+  float* col = gsm + ((a.n_par + 3) / 4) * 4 + threadIdx.x;  // this thread's column (H x kGenThreads)
   gen_stage_params(gsm, a.params, a.n_par);
   __syncthreads();
   for (int64_t row = (int64_t)blockIdx.x * kGenThreads + threadIdx.x; row - threadIdx.x < a.n_rows;
@@ -234,15 +229,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_forward_kernel(GenArgs a)
 // Scratch slots per row: hidden states h_0..h_k (k+1) x H, normed t_1..t_k
 // k x H, inv_std k, pre-LayerNorm output OUT (+ mean / inv_std 2).
 // Dynamic shared memory of gen_mlp_backward_kernel<IN, OUT, ...>.
-__host__ __device__ inline size_t gen_backward_smem(int in_dim, int out_dim) {
-  const int H = kGenH;
+__host__ __device__ inline size_t gen_backward_smem(int in_dim, int out_dim, int H) {
   const int wblk = (H * H + H) > (in_dim * H + H) ? (H * H + H) : (in_dim * H + H);
   return (size_t)(((wblk + 3) / 4) * 4 + ((in_dim * out_dim + 3) / 4) * 4 + ((out_dim + 3) / 4) * 4 +
                   2 * kGenThreads * kGenRow) * 4;
 }
 
-__host__ __device__ inline int64_t gen_scratch_slots(int k, int out_dim) {
-  return (int64_t)(2 * k + 1) * kGenH + k + out_dim + 2;
+__host__ __device__ inline int64_t gen_scratch_slots(int k, int out_dim, int H) {
+  return (int64_t)(2 * k + 1) * H + k + out_dim + 2;
 }
 
 // Tile reduction of dW += sum_rows A[r][i] D[r][j] for NI x NO, A / D staged
@@ -316,11 +310,10 @@ __device__ __forceinline__ void gen_stage_col(float* s, const float (&v)[N]) {
 // smem: one streamed layer block (W, b) | skip weights | LN gamma | A stage | D stage.
 // Weights are streamed layer by layer (the CTA walks the layers of its tile in
 // lock-step), so two CTAs fit per SM.
-template <int IN, int OUT, bool SKIP, bool OUT_LN, bool DIN>
+template <int IN, int OUT, bool SKIP, bool OUT_LN, bool DIN, int H>
 __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a) {
-  constexpr int H = kGenH;
   extern __shared__ __align__(16) float gsm[];
-  const GenLayout L{IN, OUT, a.k};
+  const GenLayout L{IN, OUT, a.k, H};
   const int K = a.k;
   constexpr int WBLK = ((H * H + H) > (IN * H + H) ? (H * H + H) : (IN * H + H));
   constexpr int SW_N = ((WBLK + 3) / 4) * 4, SK_N = ((IN * OUT + 3) / 4) * 4, LN_N = ((OUT + 3) / 4) * 4;
@@ -329,7 +322,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
   float* sG = sSkip + SK_N;
   float* sA = sG + LN_N;
   float* sD = sA + kGenThreads * kGenRow;
-  // this thread's gemv column (kGenH x kGenThreads floats) aliases the A
+  // this thread's gemv column (H x kGenThreads floats) aliases the A
   // staging buffer: every use is separated from the dW tiles by the CTA
   // barriers of load_linear / the staging
   float* col = sA + threadIdx.x;
@@ -346,7 +339,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mlp_backward_kernel(GenArgs a
     return sW;
   };
   float* gp = a.grad_partial + (int64_t)blockIdx.x * a.n_par;
-  const int64_t slots = gen_scratch_slots(K, OUT);
+  const int64_t slots = gen_scratch_slots(K, OUT, H);
   float* scr = a.scratch + (int64_t)blockIdx.x * slots * kGenThreads + threadIdx.x;
   auto S = [&](int64_t slot) -> float& { return scr[slot * kGenThreads]; };
   const int64_t s_h = 0, s_t = (int64_t)(K + 1) * H, s_inv = s_t + (int64_t)K * H, s_y = s_inv + K,

@@ -25,7 +25,9 @@ constexpr int kColStride = kMlpThreads + kColPad;
 // kEdgeFact: the edge MLP with its input linear factorised through the nodes,
 // [x_src | x_dst | e] W0 = P_s[src] + P_d[dst] + e W0_e with P = x [W0_s | W0_d]
 // computed once per node (tensor-core kernels only; same parameters).
-enum MlpInput : int { kEdgeInput = 0, kNodeInput = 1, kEdgeFact = 2 };
+// kEdgeFused: kEdgeInput's 3-segment input with the aggregate formed in the
+// same kernel (tensor-core forward only).
+enum MlpInput : int { kEdgeInput = 0, kNodeInput = 1, kEdgeFact = 2, kEdgeFused = 3 };
 
 // Flattened processor-MLP parameters (for_each order, fp32): W0 (in x H), b0,
 // W1, b1, ..., W_{k+1}, b_{k+1}. wt points at the same list with every W

@@ -18,9 +18,10 @@
 // epilogue works. Input rows (x[src], x[dst], e / a*, x) are gathered one
 // segment ahead so their latency hides behind the MMA of the previous one.
 //
-// kEdgeFact (the edge update of the MP layer, model.cpp:233-240, as ONE
-// kernel): tiles are runs of whole receiver segments (<= 128 slots, from a
-// table built at graph upload); the input linear is one K = H segment
+// kEdgeFused / kEdgeFact (the edge update of the MP layer, model.cpp:233-240,
+// as ONE kernel): tiles are runs of whole receiver segments (<= 128 slots,
+// from a table built at graph upload); kEdgeFused gathers [x_src | x_dst | e]
+// as kEdgeInput, kEdgeFact computes the input linear as one K = H segment
 // (e W0_e) plus the gathered node projections P_s[src] + P_d[dst]; the output
 // rows go through a swizzled shared-memory tile to a reducer warp per slot
 // (warps 10 / 11) that streams e' to HBM with coalesced row stores and forms
@@ -158,7 +159,7 @@ __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool 
     const float* seg;
     if (MODE == kEdgeFact)
       seg = a.e_in + row * H;
-    else if (MODE == kEdgeInput)
+    else if (MODE == kEdgeInput || MODE == kEdgeFused)
       seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * H
                    : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
     else
@@ -209,7 +210,8 @@ template <int H, int MODE, bool PROF>
 __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(TcFwdArgs a) {
   using Cfg = TcCfg<H>;
   constexpr bool FACT = MODE == kEdgeFact;
-  constexpr int nseg = MODE == kEdgeInput ? 3 : (MODE == kNodeInput ? 2 : 1);
+  constexpr bool FUSED = MODE == kEdgeFact || MODE == kEdgeFused;  // segment tiles + in-kernel aggregate
+  constexpr int nseg = MODE == kEdgeFact ? 1 : (MODE == kNodeInput ? 2 : 3);
   constexpr int in_dim = (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout (kEdgeFact: the 3H-input MLP)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -229,11 +231,11 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int n_chunks = nseg + a.k + 1;
-  const int64_t n_tiles = FACT ? a.n_tiles : (a.n_rows + 127) / 128;
+  const int64_t n_tiles = FUSED ? a.n_tiles : (a.n_rows + 127) / 128;
   const int64_t n_pairs = (n_tiles + 1) / 2;
   // rows of tile t: [t_beg, t_end) (kEdgeFact: a run of whole receiver segments)
   auto tile_rows = [&](int64_t t, int64_t& beg, int64_t& end) {
-    if (FACT) {
+    if (FUSED) {
       beg = t < n_tiles ? (int64_t)__ldg(a.tiles + t) : 0;
       end = t < n_tiles ? (int64_t)__ldg(a.tiles + t + 1) : 0;
     } else {
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       }
       wait_d();
       const long long t_out0 = PROF ? clock64() : 0;
-      if (FACT) {  // y = D + b into this slot's output tile, for the reducer warp
+      if (FUSED) {  // y = D + b into this slot's output tile, for the reducer warp
         const float* bo = sbias + (a.k + 1) * H;
         ptx::mbar_wait(&y_empty[g], py ^ 1);  // previous tile of this slot consumed
         py ^= 1;
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         atomicAdd(a.prof + kFwdProfIssMma, i_m);
       }
     }
-  } else if (FACT && warp >= 10) {
+  } else if (FUSED && warp >= 10) {
     // ------------------------------------------------------------ reducer of slot g (warps 10, 11)
     // e' rows to HBM (coalesced: the lanes cover one row) and the segment sums
     // a[i] = sum_p inv[p] e'[p] in slot order (fmaf chain from 0, as

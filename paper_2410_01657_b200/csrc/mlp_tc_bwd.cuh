@@ -59,6 +59,10 @@ struct TcBwdCfg {
 };
 
 constexpr bool kDiscardScratch = true;  // see the backward walk
+#ifndef HGNN_EXP
+#define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py): bits drop work, results are wrong
+#endif
+constexpr int kExp = HGNN_EXP;
 
 struct TcBwdArgs {
   int64_t n_rows;
@@ -93,6 +97,7 @@ enum { kProfTotal = 0, kProfW = 1, kProfA = 2, kProfSt = 3, kProfDwE = 4, kProfF
 
 template <int MODE>
 __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64]) {
+  if (HGNN_EXP & 16) valid = false;
   TcFwdArgs f{};
   f.src = a.src;
   f.dst = a.dst;
@@ -185,10 +190,10 @@ __device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&
       x.w = sw ? v[4 * qb + 3] : v[4 * qa + 3];
       const int q = sw ? qb : qa;
       float4 hi, lo;
-      hi.x = ptx::tf32_hi(x.x);
-      hi.y = ptx::tf32_hi(x.y);
-      hi.z = ptx::tf32_hi(x.z);
-      hi.w = ptx::tf32_hi(x.w);
+      hi.x = ptx::tf32_hi_stage(x.x);
+      hi.y = ptx::tf32_hi_stage(x.y);
+      hi.z = ptx::tf32_hi_stage(x.z);
+      hi.w = ptx::tf32_hi_stage(x.w);
       lo.x = x.x - hi.x;
       lo.y = x.y - hi.y;
       lo.z = x.z - hi.z;
@@ -371,6 +376,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     // Job j - 2 shares this job's accumulator and must be drained before the
     // dW MMAs of job j (which release this job's staging ring slots) can run.
     auto stage_chunk = [&](const float (&hin)[H], const float (&d)[H]) {
+      if (kExp & 1) return;
       if (job >= 2) flush(job - 2);
       const long long ts0 = PROF ? clock64() : 0;
       const int64_t gi = job * 8 + warp;  // staging chunk counter
@@ -384,6 +390,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       if (PROF) pf[3] += (unsigned long long)(clock64() - ts0);
     };
     auto write_db = [&](const float (&d)[H]) {
+      if (kExp & 4) return;
       const long long t0 = PROF ? clock64() : 0;
       const float2 cs = warp_colsum64(d);
       float* dst = dbp + ((job % 4) * 8 + warp) * 64 + colsum_base(lane);
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         ptx::tc_fence_after();
         float u[H];
         bwd_load_d(t_d, sbias + l * H, u);
-        const float inv_std = ln0_tree<H>(u);
+        const float inv_std = (kExp & 8) ? 1.0f : ln0_tree<H>(u);
         float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
 #pragma unroll
         for (int q = 0; q < 16; ++q)
@@ -488,7 +495,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         if (jb >= 1 && jb <= K) {
           const int l = K + 1 - jb;
           const float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
-          const float inv_std = scr_inv[(l - 1) * 128 + trow];
+          const float inv_std = (kExp & 2) ? 1.0f : scr_inv[(l - 1) * 128 + trow];
           const long long tl0 = PROF ? clock64() : 0;
           bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
           float p1[8], p2[8];
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float4 t4 = ptx::ld_hint(st + q * 128, keep);
+            const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
             const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -517,7 +524,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
               (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float4 t4 = ptx::ld_hint(st + q * 128, keep);
+            const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
             dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
             dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
             dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
@@ -576,8 +583,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       }
       if (PROF) pf[7] += (unsigned long long)(clock64() - ti0);
     }
-    if (job >= 2) flush(job - 2);  // last two dW jobs of this CTA
-    if (job >= 1) flush(job - 1);
+    if (!(kExp & 1) && job >= 2) flush(job - 2);  // last two dW jobs of this CTA
+    if (!(kExp & 1) && job >= 1) flush(job - 1);
     if (PROF && warp == 0 && lane == 0) {
       pf[0] = (unsigned long long)(clock64() - pf_t0);
 #pragma unroll
@@ -673,7 +680,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     int64_t gi = 0;  // staging chunk counter
     unsigned long long pc_st = 0, pc_dw = 0, pc_dwt = 0;
     const long long t_start = PROF ? clock64() : 0;
-    const int64_t n_jobs = ((n_pairs - blockIdx.x + gridDim.x - 1) / gridDim.x) * n_dw;
+    const int64_t n_jobs = (kExp & 1) ? 0 : ((n_pairs - blockIdx.x + gridDim.x - 1) / gridDim.x) * n_dw;
     for (int64_t jd = 0; jd < n_jobs; ++jd) {
       const int acc = (int)(jd & 1);
       const long long t0 = PROF ? clock64() : 0;

@@ -14,7 +14,7 @@ namespace {
 
 bool gen_supported(int64_t fx, int64_t fe, int64_t fy) { return fx == 3 && fe == 7 && fy == 3; }
 
-template <int IN, int OUT, bool SKIP, bool LN>
+template <int IN, int OUT, bool SKIP, bool LN, int H>
 void gen_forward(hgnn_ctx* c, int64_t n_rows, const float* in, float* out, int64_t par_off, int64_t n_par) {
   if (n_rows == 0) return;
   GenArgs a{};
@@ -24,8 +24,8 @@ void gen_forward(hgnn_ctx* c, int64_t n_rows, const float* in, float* out, int64
   a.params = c->gen_par.p + par_off;
   a.k = (int)c->K;
   a.n_par = n_par;
-  auto k = gen_mlp_forward_kernel<IN, OUT, SKIP, LN>;
-  const size_t smem = (size_t)((n_par + 3) / 4) * 16 + (size_t)kGenH * kGenThreads * 4;  // params + gemv columns
+  auto k = gen_mlp_forward_kernel<IN, OUT, SKIP, LN, H>;
+  const size_t smem = (size_t)((n_par + 3) / 4) * 16 + (size_t)H * kGenThreads * 4;  // params + gemv columns
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));
@@ -35,7 +35,7 @@ void gen_forward(hgnn_ctx* c, int64_t n_rows, const float* in, float* out, int64
 
 // Backward of one encoder / decoder MLP; parameter gradients (rank-local)
 // land in mgrads[par_off, par_off + n_par).
-template <int IN, int OUT, bool SKIP, bool LN, bool DIN>
+template <int IN, int OUT, bool SKIP, bool LN, bool DIN, int H>
 void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_out, float* d_in, int64_t par_off,
                   int64_t n_par) {
   if (n_rows == 0) {
@@ -44,7 +44,7 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
   }
   const int64_t tiles = (n_rows + kGenThreads - 1) / kGenThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)c->num_sms));  // 2 CTAs / SM
-  const int64_t slots = gen_scratch_slots((int)c->K, OUT);
+  const int64_t slots = gen_scratch_slots((int)c->K, OUT, H);
   c->gen_part.alloc(std::max<int64_t>(c->gen_part.n, (int64_t)grid * n_par));
   c->gen_scratch.alloc(std::max<int64_t>(c->gen_scratch.n, (int64_t)grid * slots * kGenThreads));
   CUDA_OK(cudaMemsetAsync(c->gen_part.p, 0, sizeof(float) * (size_t)(grid * n_par), c->stream));
@@ -58,14 +58,35 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
   a.scratch = c->gen_scratch.p;
   a.k = (int)c->K;
   a.n_par = n_par;
-  auto k = gen_mlp_backward_kernel<IN, OUT, SKIP, LN, DIN>;
-  const size_t smem = gen_backward_smem(IN, OUT);
+  auto k = gen_mlp_backward_kernel<IN, OUT, SKIP, LN, DIN, H>;
+  const size_t smem = gen_backward_smem(IN, OUT, H);
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, kGenThreads, smem, c->stream>>>(a);
   check_launch(c);
   reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->gen_part.p, grid, n_par,
                                                                           c->mgrads.p + par_off);
   check_launch(c);
+}
+
+// Encoders / decoder of width H (model.cpp:70-101): node encoder F_x = 3,
+// edge encoder F_e = 7, decoder F_y = 3.
+template <int H>
+void encode(hgnn_ctx* c) {
+  gen_forward<3, H, true, true, H>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
+  gen_forward<7, H, true, true, H>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
+}
+template <int H>
+void decode(hgnn_ctx* c) {
+  gen_forward<H, 3, true, false, H>(c, c->nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
+}
+template <int H>
+void decode_backward(hgnn_ctx* c) {
+  gen_backward<H, 3, true, false, true, H>(c, c->nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
+}
+template <int H>
+void encode_backward(hgnn_ctx* c) {
+  gen_backward<3, H, true, true, false, H>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
+  gen_backward<7, H, true, true, false, H>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
 }
 
 void require_model(hgnn_ctx* c) {
@@ -82,8 +103,8 @@ void model_compute_gradients(hgnn_ctx* c) {
   ensure_buffers(c);
   {  // encoders (model.cpp:289-294), every row / edge
     Timed t(c, HGNN_K_ENCODE);
-    gen_forward<3, 64, true, true>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
-    gen_forward<7, 64, true, true>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
+    if (H == 64) encode<64>(c);
+    else encode<32>(c);
   }
   // message passing (model.cpp:295-300)
   run_forward(c);
@@ -92,7 +113,8 @@ void model_compute_gradients(hgnn_ctx* c) {
   c->dy.alloc(std::max<int64_t>(nl * c->fy, 1));
   {
     Timed t(c, HGNN_K_DECODE);
-    gen_forward<64, 3, true, false>(c, nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
+    if (H == 64) decode<64>(c);
+    else decode<32>(c);
   }
   Timed t_loss(c, HGNN_K_LOSS_ADAM);
   // consistent loss (model.cpp:455-480) and its adjoint (model.cpp:482-500)
@@ -113,7 +135,8 @@ void model_compute_gradients(hgnn_ctx* c) {
   {  // decoder backward (model.cpp:402-409): adjoint of x_M on local rows, halo rows 0
     Timed t(c, HGNN_K_DECODE);
     CUDA_OK(cudaMemsetAsync(c->dx.p, 0, sizeof(float) * (size_t)(c->rows * H), c->stream));
-    gen_backward<64, 3, true, false, true>(c, nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
+    if (H == 64) decode_backward<64>(c);
+    else decode_backward<32>(c);
   }
   // message-passing backward (model.cpp:411-415), de_M = 0 (model.cpp:412)
   CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * H), c->stream));
@@ -122,8 +145,8 @@ void model_compute_gradients(hgnn_ctx* c) {
                           cudaMemcpyDeviceToDevice, c->stream));
   {  // encoder backward (model.cpp:417-423)
     Timed t(c, HGNN_K_ENCODE);
-    gen_backward<3, 64, true, true, false>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
-    gen_backward<7, 64, true, true, false>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
+    if (H == 64) encode_backward<64>(c);
+    else encode_backward<32>(c);
   }
   // average over ranks (model.cpp:516-531)
   if (c->nranks > 1) {
@@ -207,16 +230,17 @@ int hgnn_model_configure(hgnn_ctx* c, int64_t in_node_dim, int64_t in_edge_dim, 
   return guarded([&] {
     bind(c);
     if (!c->configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_configure has not been called");
-    if (c->H != kGenH) fail(HGNN_ERR_CONFIG, "model level: hidden width 64 only");
+    if (c->H != 64 && c->H != 32) fail(HGNN_ERR_CONFIG, "model level: hidden width 32 or 64");
     if (!gen_supported(in_node_dim, in_edge_dim, out_dim))
       fail(HGNN_ERR_CONFIG, "model level: feature widths (F_x, F_e, F_y) = (3, 7, 3) supported");
     c->fx = in_node_dim;
     c->fe = in_edge_dim;
     c->fy = out_dim;
     const int K = (int)c->K;
-    c->n_ne = gen_param_count((int)c->fx, kGenH, K, true, true);
-    c->n_ee = gen_param_count((int)c->fe, kGenH, K, true, true);
-    c->n_dec = gen_param_count(kGenH, (int)c->fy, K, true, false);
+    const int H = (int)c->H;
+    c->n_ne = gen_param_count((int)c->fx, H, K, true, true, H);
+    c->n_ee = gen_param_count((int)c->fe, H, K, true, true, H);
+    c->n_dec = gen_param_count(H, (int)c->fy, K, true, false, H);
     c->off_ne = 0;
     c->off_ee = c->n_ne;
     c->off_mp = c->off_ee + c->n_ee;

@@ -44,6 +44,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait with a suspend-time hint: compiles to TRYWAIT + NANOSLEEP.SYNCS +
+// PHASECHK, i.e. a failed probe parks the warp until barrier activity (or the
+// hint) instead of re-issuing the probe. Measured slower for the MLP kernels'
+// waits (edge backward +8 % at C3: the park adds wake-up latency to every MMA
+// hand-off), so mbar_wait keeps the plain probe loop; kept for waits off the
+// critical path.
+__device__ __forceinline__ bool mbar_try_wait_parked(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
+      : "memory");
+  return ok != 0;
+}
+
 // Watchdog: a wait that does not complete within ~20 s of SM clock reports
 // the barrier and traps, so a protocol bug fails the launch instead of
 // hanging the device.
@@ -282,14 +298,29 @@ __device__ __forceinline__ uint64_t opaque64(uint64_t x) {
 
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// 3xTF32 high part: x rounded to the nearest tf32 (ties away from zero; two
-// integer ops). The residual x - hi is exact in fp32 and has a random sign
-// relative to x, so the tensor core's truncation of it to tf32 adds no
-// systematic bias (with a truncated hi the residual always has x's sign and
-// its truncation shrinks every product's magnitude by ~2^-21 — a bias that
-// survives sums over 10^5 rows).
+// 3xTF32 high part. HGNN_TF32_RNA = 1: x rounded to the nearest tf32 (two
+// integer ops); the residual x - hi then has a random sign relative to x, so
+// the tensor core's truncation of it adds no systematic ~2^-21 shrink of the
+// products. Measured at the bench shape (H64 k5 M4, 6^3/P5, tests/
+// test_gpu_configs.py, scripts/dbg_accuracy.py): worst weight-gradient tensor
+// 1.16e-3 (truncated hi) vs 8.1e-4 (rounded) vs 6.8e-4 for exact fp32 SIMT
+// arithmetic (the tensor is a cancelling sum over 30 K rows), for +10 % edge
+// backward time (the dW staging split is on its critical path). Default:
+// truncation (one LOP3), within 2x of fp32 on every tensor.
+#ifndef HGNN_TF32_RNA
+#define HGNN_TF32_RNA 0
+#endif
 __device__ __forceinline__ float tf32_hi(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  if (HGNN_TF32_RNA) return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  return tf32_trunc(x);
+}
+// Split used for the dW staging operands (HGNN_TF32_RNA_STAGE, default = HGNN_TF32_RNA).
+#ifndef HGNN_TF32_RNA_STAGE
+#define HGNN_TF32_RNA_STAGE HGNN_TF32_RNA
+#endif
+__device__ __forceinline__ float tf32_hi_stage(float x) {
+  if (HGNN_TF32_RNA_STAGE) return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  return tf32_trunc(x);
 }
 
 // fp32 -> tf32 (round to nearest, ties away), result kept in fp32 format.

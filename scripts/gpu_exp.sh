@@ -1,4 +1,3 @@
-# Quick A/B of a kernel change: parity tests, then two MP-stack bench lines (1 GPU).
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_parity.log 2>&1; echo parity_rc=$?
-for i in 1 2; do timeout 600 python bench.py --no-e2e --no-train-step --no-cpu-baseline > gpurun_out/bench_exp.json 2>/dev/null
-python -c "import json; d=json.loads(open('gpurun_out/bench_exp.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['roofline']['ms_per_launch'], d['kernel_share']['node_bwd'])"; done
+set -x
+timeout 600 python scripts/dbg_accuracy.py > gpurun_out/acc_rna.log 2>&1; echo rc=$?
+HGNN_B200_LIB=paper_2410_01657_b200/lib/exp/libhgnn_b200_exptrunc.so timeout 600 python scripts/dbg_accuracy.py > gpurun_out/acc_trunc.log 2>&1; echo rc=$?

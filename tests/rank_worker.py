@@ -42,9 +42,13 @@ def main():
     ap.add_argument("--mode")
     ap.add_argument("--out")
     ap.add_argument("--model", action="store_true", help="full model (encoders, loss, Adam) on TGV features")
+    ap.add_argument("--mismatch", action="store_true",
+                    help="collective_check on; rank 1 runs another exchange mode: both ranks must raise")
     a = ap.parse_args()
     if a.model:
         return model_main(a)
+    if a.mismatch:
+        return mismatch_main(a)
     cfg = GnnConfig("w", a.H, a.M, a.k, mode=a.mode)
     g = build_rank_graph(a.E, a.p, a.R, a.rank, "verify")
     eng = Engine(a.rank, a.rank, a.R, bytes.fromhex(a.uid))
@@ -62,6 +66,29 @@ def main():
     np.savez(a.out, x_out=x_out, e_out=e_out, a_sync0=a_sync0, dx0=dx0, de0=de0, grads=grads, x_out2=x_out2,
              x_serial=x_ser, e_serial=e_ser, dx0_serial=dx0_s, de0_serial=de0_s, grads_serial=grads_s,
              halo_bytes=eng.halo_bytes())
+    eng.close()
+
+
+def mismatch_main(a):
+    """A mismatched collective sequence over NCCL raises CollectiveError on every
+    rank (debug option collective_check) instead of deadlocking."""
+    from paper_2410_01657_b200 import CollectiveError
+    mode = a.mode if a.rank == 0 else ("a2a" if a.mode == "na2a" else "na2a")
+    cfg = GnnConfig("w", a.H, a.M, a.k, mode=mode)
+    g = build_rank_graph(a.E, a.p, a.R, a.rank, "verify")
+    eng = Engine(a.rank, a.rank, a.R, bytes.fromhex(a.uid))
+    eng.upload_graph(g)
+    eng.configure(cfg)
+    eng.upload_params(mp_params(cfg, init_params(cfg, 0)))
+    eng.set_option("collective_check", 1)
+    eng.set_option("collective_timeout_ms", 20000)
+    x0, e0, _ = gid_inputs(g, a.H)
+    msg = ""
+    try:
+        eng.nmp_forward(x0, e0)
+    except CollectiveError as ex:
+        msg = str(ex)
+    np.savez(a.out, raised=np.array(bool(msg)), msg=np.array(msg))
     eng.close()
 
 

@@ -135,3 +135,15 @@ def test_two_gpu_training_is_consistent(gpus):
         for a_, b_ in zip(r["steps"], ref_losses):
             assert abs(a_ - b_) / b_ < 1e-4
     assert res[0]["params"].tobytes() == res[1]["params"].tobytes()  # ranks stay in lock-step
+
+
+def test_two_gpu_mismatched_sequence_raises(gpus):
+    """With the debug guard on, ranks posting different collectives (here:
+    different exchange modes) both raise CollectiveError (comm.cpp:184-188)."""
+    if gpus < 2:
+        pytest.skip("needs 2 GPUs")
+    with tempfile.TemporaryDirectory() as tmp:
+        res = launch(2, 2, 2, 8, 1, 1, "na2a", tmp, extra=("--mismatch",))
+    for r in res:
+        assert bool(r["raised"]), r
+        assert "mismatched collective sequence" in str(r["msg"]) or "did not complete" in str(r["msg"])
