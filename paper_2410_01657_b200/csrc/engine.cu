@@ -197,33 +197,90 @@ bool tc_eligible(const hgnn_ctx* c) { return c->H == 32 || c->H == 64; }
 // --------------------------------------------------------------------------
 // buffers
 // --------------------------------------------------------------------------
+bool use_fact(const hgnn_ctx* c);
+bool use_tc_bwd(const hgnn_ctx* c);
+
+// Activation / adjoint buffers of the MP stack under the standard or the
+// memory-lean plan (hgnn_ctx::lean). Per rank, node = rows x H, edge = N_e x H
+// fp32 tensors:
+//   standard  x_0..M, a*_0..M-1, dx, dx_seed, d_a, dx_node     (2M + 5) node
+//             e_0..M, de, dY (or d_src + d_dst)                 (M + 3 or 4) edge
+//             node projections per layer (factorised)          2M node
+//   lean      x_0..M-1 (x_M in dY), a*, dx (= dx_node), d_a    (2M + 2) node
+//             e_0..M-1 (de_m over e_m), dY                      (M + 1) edge, 2 node
 void ensure_buffers(hgnn_ctx* c) {
   if (!c->configured) fail(HGNN_ERR_UNINITIALIZED, "hgnn_configure has not been called");
   if (!c->graph_ready) fail(HGNN_ERR_UNINITIALIZED, "hgnn_graph_upload has not been called");
   const int64_t H = c->H, M = c->M;
-  if (c->xs.size() != (size_t)(M + 1) || (c->xs.size() && c->xs[0]->n != c->rows * H) ||
-      (c->es.size() && c->es[0]->n != c->ne * H)) {
+  const int64_t node = c->rows * H * 4, edge = std::max<int64_t>(1, c->ne * H) * 4;
+  const bool lean_ok = c->fact_ok && H == 64 && c->bwd_impl == 1 && c->fwd_impl == 1 && M > 0;
+  auto release = [&] {
     c->xs.clear();
     c->es.clear();
     c->as.clear();
+    c->ps.clear();
+    c->dx.release();
+    c->dx_in.release();
+    c->d_a.release();
+    c->dxn.release();
+    c->de.release();
+    c->dsrc.release();
+    c->ddst.release();
+    for (auto& v : c->plan_key) v = -1;
+  };
+  bool lean = c->lean_opt == 1;
+  if (c->lean_opt == 1 && !lean_ok)
+    fail(HGNN_ERR_CONFIG, "memory_lean needs the tcgen05 forward / backward at H = 64 (factorised edge path)");
+  if (c->lean_opt == -1 && lean_ok) {
+    const int64_t fact_ps = (c->edge_fact && c->fact_ok && H == 64) ? 2 * M * node : 0;
+    const int64_t standard = (2 * M + 5) * node + (M + (c->edge_fact ? 3 : 4)) * edge + fact_ps;
+    const bool same = c->plan_key[0] == H && c->plan_key[1] == M && c->plan_key[2] == c->rows &&
+                      c->plan_key[3] == c->ne;
+    if (!same) {  // (re)plan against the free device memory
+      release();
+      size_t free_b = 0, total_b = 0;
+      CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+      lean = (double)standard > 0.94 * (double)free_b;
+    } else {
+      lean = c->plan_key[4] == 1;
+    }
+  }
+  if (lean) c->edge_fact = 1;  // the lean plan has no per-edge d_x_dst / d_x_src tensors
+  const bool fact = c->edge_fact && c->fact_ok && H == 64;
+  const int64_t key[6] = {H, M, c->rows, c->ne, lean ? 1 : 0, fact ? 1 : 0};
+  if (!std::equal(key, key + 6, c->plan_key)) {
+    release();
+    std::copy(key, key + 6, c->plan_key);
+    c->lean = lean;
+    c->forward_done = false;
     for (int64_t m = 0; m <= M; ++m) {
-      c->xs.emplace_back(new DevBuf<float>());
-      c->xs.back()->alloc(c->rows * H);
-      c->es.emplace_back(new DevBuf<float>());
-      c->es.back()->alloc(std::max<int64_t>(1, c->ne * H));
+      if (!(lean && m == M)) {
+        c->xs.emplace_back(new DevBuf<float>());
+        c->xs.back()->alloc(c->rows * H);
+        c->es.emplace_back(new DevBuf<float>());
+        c->es.back()->alloc(std::max<int64_t>(1, c->ne * H));
+      }
       if (m < M) {
         c->as.emplace_back(new DevBuf<float>());
         c->as.back()->alloc(c->rows * H);
       }
     }
     c->dx.alloc(c->rows * H);
-    c->dx_in.alloc(c->rows * H);
     c->d_a.alloc(c->rows * H);
-    c->dxn.alloc(std::max<int64_t>(1, c->nl * H));
-    c->de.alloc(std::max<int64_t>(1, c->ne * H));
-    c->dsrc.alloc(std::max<int64_t>(1, c->ne * H));
-    c->ddst.alloc(std::max<int64_t>(1, c->ne * H));
+    c->dsrc.alloc(std::max<int64_t>({1, c->ne * H, lean ? c->rows * H : 0}));
+    if (!lean) {
+      c->dx_in.alloc(c->rows * H);
+      c->dxn.alloc(std::max<int64_t>(1, c->nl * H));
+      c->de.alloc(std::max<int64_t>(1, c->ne * H));
+    }
+    if (!(fact && c->bwd_impl == 1)) c->ddst.alloc(std::max<int64_t>(1, c->ne * H));
+    for (int64_t m = 0; m < (lean ? 1 : M); ++m) {
+      c->ps.emplace_back(new DevBuf<float>());
+      if (fact) c->ps.back()->alloc(c->rows * 2 * H);
+    }
+    c->synth_valid = false;
   }
+  if (c->ddst.n == 0 && !(use_fact(c) && use_tc_bwd(c))) c->ddst.alloc(std::max<int64_t>(1, c->ne * H));
   plan_mlp(c, true, kEdgeInput, c->ne, c->grid_edge_f, c->smem_edge_f, c->wsm_edge_f);
   plan_mlp(c, false, kEdgeInput, c->ne, c->grid_edge_b, c->smem_edge_b, c->wsm_edge_b);
   plan_mlp(c, true, kNodeInput, c->nl, c->grid_node_f, c->smem_node_f, c->wsm_node_f);
@@ -235,13 +292,6 @@ void ensure_buffers(hgnn_ctx* c) {
   const int64_t n_slots = (2 * c->K + 1) * H + c->K;
   c->scratch.alloc(max_grid * n_slots * kMlpThreads);
   if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
-  if (c->ps.size() != (size_t)M || (M > 0 && c->ps[0]->n != c->rows * 2 * H)) {
-    c->ps.clear();
-    for (int64_t m = 0; m < M; ++m) {
-      c->ps.emplace_back(new DevBuf<float>());
-      if (c->edge_fact && c->fact_ok && H == 64) c->ps.back()->alloc(c->rows * 2 * H);
-    }
-  }
   if (c->ps_ready.size() != (size_t)M) c->ps_ready.assign((size_t)M, 0);
   c->fact_blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (c->rows + kFactRows - 1) / kFactRows),
                                           (int64_t)c->num_sms * 2);
@@ -603,8 +653,9 @@ void edge_proj(hgnn_ctx* c, int64_t m, const float* x) {
   constexpr size_t smem = edge_proj_smem<64>();
   CUDA_OK(cudaFuncSetAttribute(edge_proj_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)std::min<int64_t>((c->nl + kFactRows - 1) / kFactRows, (int64_t)c->num_sms * 4);
-  edge_proj_kernel<64><<<grid, kFactThreads, smem, c->stream>>>(x, w0, c->nl, c->ps[(size_t)m]->p);
+  edge_proj_kernel<64><<<grid, kFactThreads, smem, c->stream>>>(x, w0, c->nl, proj_buf(c, m));
   check_launch(c);
+  if (c->lean) std::fill(c->ps_ready.begin(), c->ps_ready.end(), 0);  // one shared buffer
   c->ps_ready[(size_t)m] = 1;
 }
 
@@ -636,7 +687,7 @@ void launch_fused_forward(hgnn_ctx* c, int64_t m, int64_t t0, int64_t t1, const 
   args.e_in = e;
   args.out = e2;
   args.agg = a;
-  args.proj = fact ? c->ps[(size_t)m]->p : nullptr;
+  args.proj = fact ? proj_buf(c, m) : nullptr;
   args.chunks = c->chunks.p + c->chunk_off[(size_t)(3 * m + (fact ? 2 : 0))];
   args.params = layer_params(c, m, true).p;
   args.k = (int)c->K;
@@ -752,11 +803,11 @@ void layer_forward_fused(hgnn_ctx* c, int64_t m, float* x, float* e, float* e2, 
 
 void layer_forward(hgnn_ctx* c, int64_t m) {
   const int64_t H = c->H;
-  float* x = c->xs[m]->p;
-  float* e = c->es[m]->p;
-  float* e2 = c->es[m + 1]->p;
+  float* x = x_buf(c, m);
+  float* e = e_buf(c, m);
+  float* e2 = e_buf(c, m + 1);  // nullptr: the dead last-layer e' (lean plan, fused path only)
   float* a = c->as[m]->p;
-  float* x2 = c->xs[m + 1]->p;
+  float* x2 = x_buf(c, m + 1);
   if (use_fused_fwd(c)) {
     layer_forward_fused(c, m, x, e, e2, a, x2);
     return;
@@ -845,8 +896,11 @@ void reduce_grads(hgnn_ctx* c, int grid, int64_t n_par, double* out) {
 // adjoint (c->dx) and de the edge input adjoint (in place).
 void layer_backward(hgnn_ctx* c, int64_t m) {
   const int64_t H = c->H;
-  float* x = c->xs[m]->p;
-  float* e = c->es[m]->p;
+  float* x = x_buf(c, m);
+  float* e = e_buf(c, m);
+  const float* de_in = de_in_buf(c, m);
+  float* de_out = de_out_buf(c, m);
+  float* dxn = dxn_buf(c);
   float* a = c->as[m]->p;
   const int64_t goff = m * (c->n_edge_par + c->n_node_par);
   {  // node update backward (model.cpp:326-340)
@@ -861,7 +915,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.a = a;
       args.d_out = c->dx.p;
       args.d_a_out = c->d_a.p;
-      args.d_x_out = c->dxn.p;
+      args.d_x_out = dxn;
       args.grad_partial = c->grad_part.p;
       if (c->nl > 0) {
         launch_tc_backward(c, kNodeInput, m, args);
@@ -875,7 +929,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.a = a;
       args.d_out = c->dx.p;
       args.d_a_out = c->d_a.p;
-      args.d_x_out = c->dxn.p;
+      args.d_x_out = dxn;
       args.grad_partial = c->grad_part.p;
       args.scratch = c->scratch.p;
       args.n_slots = (2 * c->K + 1) * H + c->K;
@@ -915,10 +969,11 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.e_in = e + s0 * H;
       args.inv_deg = c->inv.p + s0;
       args.d_a = c->d_a.p;
-      args.de_io = c->de.p + s0 * H;
+      args.de_in = de_in ? de_in + s0 * H : nullptr;
+      args.de_io = de_out + s0 * H;
       args.d_src = c->dsrc.p + s0 * H;
       args.d_dst = c->ddst.p + s0 * H;
-      args.proj = fact ? c->ps[(size_t)m]->p : nullptr;
+      args.proj = fact ? proj_buf(c, m) : nullptr;
       args.dy_out = c->dsrc.p + s0 * H;  // kEdgeFact: dY
       args.grad_partial = part;
       return args;
@@ -963,10 +1018,11 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.e_in = e;
       args.inv_deg = c->inv.p;
       args.d_a = c->d_a.p;
-      args.de_io = c->de.p;
+      args.de_in = de_in;
+      args.de_io = de_out;
       args.d_src = c->dsrc.p;
       args.d_dst = c->ddst.p;
-      args.proj = fact ? c->ps[(size_t)m]->p : nullptr;
+      args.proj = fact ? proj_buf(c, m) : nullptr;
       args.dy_out = c->dsrc.p;  // kEdgeFact: dY
       args.grad_partial = c->grad_part.p;
       if (c->ne > 0) {
@@ -983,7 +1039,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
       args.e_in = e;
       args.inv_deg = c->inv.p;
       args.d_a = c->d_a.p;
-      args.de_io = c->de.p;
+      args.de_io = c->de.p;  // SIMT path: standard plan only (in place)
       args.d_src = c->dsrc.p;
       args.d_dst = c->ddst.p;
       args.grad_partial = c->grad_part.p;
@@ -1001,7 +1057,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
     CUDA_OK(cudaFuncSetAttribute(edge_input_adjoint_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     edge_input_adjoint_kernel<64><<<c->fact_blocks, kFactThreads, smem, c->stream>>>(
-        c->dsrc.p, x, c->dxn.p, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
+        c->dsrc.p, x, dxn, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
     check_launch(c);
     const int64_t nw = 2 * H * H;  // W0 rows 0 .. 2H-1 (x_src, x_dst blocks) of the edge MLP
     grad_reduce_add_kernel<<<blocks_for(nw), kEwThreads, 0, c->stream>>>(c->fact_part.p, c->fact_blocks, nw,
@@ -1010,7 +1066,7 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
   } else {  // input-node adjoint (model.cpp:378-386)
     Timed t(c, HGNN_K_DX);
     dx_gather_kernel<<<blocks_for(c->rows * H / 4), kEwThreads, 0, c->stream>>>(
-        c->dsrc.p, c->ddst.p, c->dxn.p, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, (int)H, c->dx.p);
+        c->dsrc.p, c->ddst.p, dxn, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, (int)H, c->dx.p);
     check_launch(c);
   }
 }
@@ -1026,6 +1082,7 @@ void run_backward(hgnn_ctx* c) {
   if (c->M == 0) return;
   CUDA_OK(cudaMemsetAsync(c->grads.p, 0, sizeof(double) * (size_t)c->n_mp_par, c->stream));
   for (int64_t m = c->M - 1; m >= 0; --m) layer_backward(c, m);
+  if (c->lean) c->forward_done = false;  // de_m overwrote e_m, dY overwrote x_M
 }
 
 void require_ready(hgnn_ctx* c) {
@@ -1457,11 +1514,12 @@ int hgnn_mp_forward(hgnn_ctx* c, const double* x0, const double* e0, double* x_o
     require_ready(c);
     if (!x0 || !e0) fail(HGNN_ERR_SHAPE, "hgnn_mp_forward: null input");
     ensure_buffers(c);
+    if (e_out && c->lean) fail(HGNN_ERR_SIZE, "hgnn_mp_forward: e_out is not materialised under the memory-lean plan");
     rows_to_device(c, x0, c->rows * c->H, c->xs[0]->p);
     edges_to_device(c, e0, c->es[0]->p);
     run_forward(c);
-    if (x_out) rows_to_host(c, c->xs[(size_t)c->M]->p, c->rows * c->H, x_out);
-    if (e_out) edges_to_host(c, c->es[(size_t)c->M]->p, e_out);
+    if (x_out) rows_to_host(c, x_buf(c, c->M), c->rows * c->H, x_out);
+    if (e_out) edges_to_host(c, e_buf(c, c->M), e_out);
     CUDA_OK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1472,12 +1530,15 @@ int hgnn_mp_backward(hgnn_ctx* c, const double* dx, const double* de, double* dx
     require_ready(c);
     if (!dx) fail(HGNN_ERR_SHAPE, "hgnn_mp_backward: null output adjoint");
     ensure_buffers(c);
+    if (de && c->lean) fail(HGNN_ERR_SIZE, "hgnn_mp_backward: de (adjoint of e_M) needs the standard memory plan");
     rows_to_device(c, dx, c->rows * c->H, c->dx.p);
-    if (de) edges_to_device(c, de, c->de.p);
-    else CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * c->H), c->stream));
+    if (!c->lean) {
+      if (de) edges_to_device(c, de, c->de.p);
+      else CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * c->H), c->stream));
+    }
     run_backward(c);
     if (dx0) rows_to_host(c, c->dx.p, c->rows * c->H, dx0);
-    if (de0) edges_to_host(c, c->de.p, de0);
+    if (de0) edges_to_host(c, de_out_buf(c, 0), de0);
     if (grads) {
       CUDA_OK(cudaMemcpyAsync(grads, c->grads.p, sizeof(double) * (size_t)c->n_mp_par, cudaMemcpyDeviceToHost,
                               c->stream));
@@ -1492,15 +1553,38 @@ int hgnn_get_trace(hgnn_ctx* c, int layer, int which, double* out) {
     if (!c->forward_done) fail(HGNN_ERR_UNINITIALIZED, "no forward trace available");
     if (layer < 0 || layer >= c->M) fail(HGNN_ERR_SHAPE, "trace layer out of range");
     switch (which) {
-      case HGNN_TRACE_X_IN: rows_to_host(c, c->xs[(size_t)layer]->p, c->rows * c->H, out); break;
-      case HGNN_TRACE_E_IN: edges_to_host(c, c->es[(size_t)layer]->p, out); break;
+      case HGNN_TRACE_X_IN: rows_to_host(c, x_buf(c, layer), c->rows * c->H, out); break;
+      case HGNN_TRACE_E_IN: edges_to_host(c, e_buf(c, layer), out); break;
       case HGNN_TRACE_A_SYNC: rows_to_host(c, c->as[(size_t)layer]->p, c->rows * c->H, out); break;
-      case HGNN_TRACE_X_OUT: rows_to_host(c, c->xs[(size_t)layer + 1]->p, c->rows * c->H, out); break;
-      case HGNN_TRACE_E_OUT: edges_to_host(c, c->es[(size_t)layer + 1]->p, out); break;
+      case HGNN_TRACE_X_OUT: rows_to_host(c, x_buf(c, layer + 1), c->rows * c->H, out); break;
+      case HGNN_TRACE_E_OUT:
+        if (!e_buf(c, layer + 1)) fail(HGNN_ERR_SIZE, "e_out of the last layer is not stored (memory-lean plan)");
+        edges_to_host(c, e_buf(c, layer + 1), out);
+        break;
       default: fail(HGNN_ERR_CONFIG, "unknown trace selector");
     }
   });
 }
+
+}  // extern "C"
+
+namespace hgnn_b200::engine {
+// Seeded device inputs keyed by global id; what the lean plan's backward
+// consumes (e_0 storage, the dx seed) is re-created by step_device.
+void synth_edges_in(hgnn_ctx* c) {
+  if (c->ne == 0) return;
+  synth_edges_kernel<<<blocks_for(c->ne * c->H), kEwThreads, 0, c->stream>>>(
+      c->gid.p, c->src.p, c->dst.p, c->ne, (int)c->H, c->synth_seed ^ 0x5bd1e995ull, c->es[0]->p);
+  check_launch(c);
+}
+void synth_dx_seed(hgnn_ctx* c, float* dst) {
+  synth_rows_kernel<<<blocks_for(c->rows * c->H), kEwThreads, 0, c->stream>>>(
+      c->gid.p, c->rows, c->nl, (int)c->H, c->synth_seed ^ 0xc2b2ae35ull, 1e-3f, dst);
+  check_launch(c);
+}
+}  // namespace hgnn_b200::engine
+
+extern "C" {
 
 int hgnn_synthetic_inputs(hgnn_ctx* c, uint64_t seed) {
   return guarded([&] {
@@ -1508,17 +1592,13 @@ int hgnn_synthetic_inputs(hgnn_ctx* c, uint64_t seed) {
     require_ready(c);
     ensure_buffers(c);
     const int64_t H = c->H;
+    c->synth_seed = seed;
     synth_rows_kernel<<<blocks_for(c->rows * H), kEwThreads, 0, c->stream>>>(c->gid.p, c->rows, c->nl, (int)H, seed,
                                                                             1.0f, c->xs[0]->p);
     check_launch(c);
-    if (c->ne > 0) {
-      synth_edges_kernel<<<blocks_for(c->ne * H), kEwThreads, 0, c->stream>>>(c->gid.p, c->src.p, c->dst.p, c->ne,
-                                                                             (int)H, seed ^ 0x5bd1e995ull, c->es[0]->p);
-      check_launch(c);
-    }
-    synth_rows_kernel<<<blocks_for(c->rows * H), kEwThreads, 0, c->stream>>>(c->gid.p, c->rows, c->nl, (int)H,
-                                                                            seed ^ 0xc2b2ae35ull, 1e-3f, c->dx_in.p);
-    check_launch(c);
+    synth_edges_in(c);
+    if (!c->lean) synth_dx_seed(c, c->dx_in.p);
+    c->synth_valid = true;
     CUDA_OK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1528,9 +1608,11 @@ int hgnn_set_inputs(hgnn_ctx* c, const double* x0, const double* e0, const doubl
     bind(c);
     require_ready(c);
     ensure_buffers(c);
+    if (c->lean) fail(HGNN_ERR_SIZE, "hgnn_set_inputs needs the standard memory plan (use hgnn_synthetic_inputs)");
     rows_to_device(c, x0, c->rows * c->H, c->xs[0]->p);
     edges_to_device(c, e0, c->es[0]->p);
     rows_to_device(c, dx, c->rows * c->H, c->dx_in.p);
+    c->synth_valid = false;
     CUDA_OK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1540,6 +1622,14 @@ int hgnn_mp_step_device(hgnn_ctx* c) {
     bind(c);
     require_ready(c);
     ensure_buffers(c);
+    if (c->lean) {  // the previous backward wrote de_0 over e_0: re-create the inputs
+      if (!c->synth_valid) fail(HGNN_ERR_UNINITIALIZED, "memory-lean step_device needs hgnn_synthetic_inputs");
+      synth_edges_in(c);
+      run_forward(c);
+      synth_dx_seed(c, c->dx.p);
+      run_backward(c);
+      return;
+    }
     run_forward(c);
     CUDA_OK(cudaMemcpyAsync(c->dx.p, c->dx_in.p, sizeof(float) * (size_t)(c->rows * c->H), cudaMemcpyDeviceToDevice,
                             c->stream));
@@ -1576,8 +1666,11 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       c->halo_sm_reserve = (int)value;
     } else if (k == "edge_factorized") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "edge_factorized: 0 (3-segment edge kernels) or 1");
-      if (c->edge_fact != (int)value) c->ps.clear();  // (re)allocated by ensure_buffers
-      c->edge_fact = (int)value;
+      c->edge_fact = (int)value;  // buffers follow at the next ensure_buffers (plan key)
+    } else if (k == "memory_lean") {
+      if (value < -1 || value > 1) fail(HGNN_ERR_CONFIG, "memory_lean: -1 (auto), 0 or 1");
+      c->lean_opt = (int)value;
+      for (auto& v : c->plan_key) v = -1;  // re-plan at the next call
     } else if (k == "collective_check") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "collective_check: 0 or 1");
       c->coll_check = (int)value;

@@ -136,6 +136,18 @@ struct hgnn_ctx {
   hgnn_b200::DevBuf<float> fact_part;                         // node-level dW0_s / dW0_d partials
   int fact_blocks = 0;
 
+  // memory plan (option "memory_lean": -1 auto = when the standard plan does
+  // not fit the device, 0 off, 1 on). Lean: the dead last-layer e' is not
+  // stored, the edge adjoint of layer m overwrites e_m (after the backward
+  // kernel's reads of that row), one node-projection buffer recomputed per
+  // layer, the node-update x adjoint overwrites dx in place, x_M lives in the
+  // (then idle) dY buffer, and the bench's dx seed is re-synthesised.
+  int lean_opt = -1;
+  bool lean = false;
+  int64_t plan_key[6] = {-1, -1, -1, -1, -1, -1};
+  uint64_t synth_seed = 0;
+  bool synth_valid = false;
+
   // activations
   std::vector<std::unique_ptr<hgnn_b200::DevBuf<float>>> xs, es, as;
   hgnn_b200::DevBuf<float> dx, dxn, d_a, de, dsrc, ddst, dx_in;
@@ -290,6 +302,21 @@ void mp_chunk_plan(int H, int K, int64_t M, bool with_bwd, Emit&& emit, std::vec
     off = off_node + mlp_param_count(2 * H, H, K);
   }
 }
+
+// Buffer views of the memory plan (see hgnn_ctx::lean).
+inline float* x_buf(hgnn_ctx* c, int64_t m) {
+  return (c->lean && m == c->M) ? c->dsrc.p : c->xs[(size_t)m]->p;
+}
+inline float* e_buf(hgnn_ctx* c, int64_t m) {  // nullptr: not materialised (lean, m = M)
+  return (c->lean && m == c->M) ? nullptr : c->es[(size_t)m]->p;
+}
+inline const float* de_in_buf(hgnn_ctx* c, int64_t m) {  // adjoint of e_{m+1} (nullptr: zero)
+  if (!c->lean) return c->de.p;
+  return m + 1 == c->M ? nullptr : c->es[(size_t)m + 1]->p;
+}
+inline float* de_out_buf(hgnn_ctx* c, int64_t m) { return c->lean ? c->es[(size_t)m]->p : c->de.p; }
+inline float* dxn_buf(hgnn_ctx* c) { return c->lean ? c->dx.p : c->dxn.p; }
+inline float* proj_buf(hgnn_ctx* c, int64_t m) { return c->ps[c->lean ? 0 : (size_t)m]->p; }
 
 void bind(hgnn_ctx* c);
 // in-place sum over ranks of n device doubles on the compute stream (NCCL, or

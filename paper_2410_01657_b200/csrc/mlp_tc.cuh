@@ -501,15 +501,15 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
           const int32_t d = __shfl_sync(0xffffffffu, d_l, i);
           const int32_t dn = __shfl_sync(0xffffffffu, dn_l, i);
           const float w = __shfl_sync(0xffffffffu, w_l, i);
-          float* eo = a.out + (tb + r) * H + CPL * lane;
+          float* eo = a.out ? a.out + (tb + r) * H + CPL * lane : nullptr;  // nullptr: e' not stored (dead)
           if (CPL == 2) {
             const float2 y = *reinterpret_cast<const float2*>(yt + ytile_off<H>(r, lane / 2) + 8 * (lane & 1));
-            *reinterpret_cast<float2*>(eo) = y;
+            if (eo) *reinterpret_cast<float2*>(eo) = y;
             acc[0] = fmaf(w, y.x, acc[0]);
             acc[CPL - 1] = fmaf(w, y.y, acc[CPL - 1]);
           } else {
             const float y = *reinterpret_cast<const float*>(yt + ytile_off<H>(r, lane / 4) + 4 * (lane & 3));
-            *eo = y;
+            if (eo) *eo = y;
             acc[0] = fmaf(w, y, acc[0]);
           }
           if (dn != d) {  // last slot of receiver d's segment

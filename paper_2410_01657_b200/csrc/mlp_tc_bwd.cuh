@@ -8,11 +8,11 @@
 // Per CTA (persistent, one per SM), two 128-row tile slots ping-pong as in
 // the forward kernel. TMEM (512 columns):
 //   slot s: [A_hi 64 | A_lo 64 | D 64]  (s = 0, 1)      cols [192 s, 192 s + 192)
-//   dW accumulators 2 x (128 x 64), by job parity        cols [384, 448), [448, 512)
-// Per 8-row K-step the dW product is two SS MMAs into one accumulator:
-//   [h_hi^T ; h_lo^T] (128 x 8) x d_hi (8 x 64)  and  ... x d_lo (8 x 64),
-// so lanes 0-63 collect hh + hl and lanes 64-127 lh + ll (the tiny ll term is
-// kept: free and slightly more accurate). Both operands are staged per warp
+//   dW accumulator 128 x 128                               cols [384, 512)
+// Per 8-row K-step the dW product is one SS MMA (kDwN128):
+//   [h_hi^T ; h_lo^T] (128 x 8) x [d_hi | d_lo] (8 x 128),
+// so lanes 0-63 collect hh | hl and lanes 64-127 lh | ll in the two column
+// halves (the tiny ll term is kept: free and slightly more accurate). Both operands are staged per warp
 // (32 rows) in shared memory as MN-major SWIZZLE_128B_BASE32B tiles (the layout
 // tf32 MN-major operands require), through a ring of NSTAGE buffers consumed
 // in a fixed warp order (deterministic accumulation) by a dW issuer warp that
@@ -59,6 +59,16 @@ struct TcBwdCfg {
 };
 
 constexpr bool kDiscardScratch = true;  // see the backward walk
+// dW as ONE N = 128 MMA per 8-row K-step: [h_hi ; h_lo] (M = 128) x [d_hi | d_lo]
+// (N = 128) into a single 128-column accumulator (hh hl / lh ll quadrants),
+// instead of two N = 64 MMAs into two double-buffered 64-column ones: the A
+// operand is read from shared memory once instead of twice (the SS dW MMAs are
+// shared-memory-bandwidth bound), half the MMA issues. The accumulator of job j
+// is drained when the warps start staging job j + 1.
+#ifndef HGNN_DW_N128
+#define HGNN_DW_N128 1
+#endif
+constexpr bool kDwN128 = HGNN_DW_N128;
 #ifndef HGNN_EXP
 #define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py): bits drop work, results are wrong
 #endif
@@ -75,7 +85,8 @@ struct TcBwdArgs {
   const float* d_out;    // node mode: dx rows
   const float* inv_deg;  // edge mode
   const float* d_a;      // edge mode
-  float* de_io;          // edge mode: de in, de_next out (in place)
+  const float* de_in;    // edge mode: adjoint of the edge output (nullptr: zero, the last layer)
+  float* de_io;          // edge mode: adjoint of the edge input out (may alias de_in or e_in row by row)
   float* d_src;          // edge mode outputs
   float* d_dst;
   float* d_a_out;        // node mode outputs
@@ -341,15 +352,29 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const int lin = jj <= K ? K + 1 - jj : 0;
       const int rowbase = jj <= K ? 0 : (jj - K - 1 + seg0) * H;
       const bool with_db = jj <= K + 1;
-      const int acc = (int)(jf & 1);
-      ptx::mbar_wait(&dw_full[acc], (uint32_t)((jf >> 1) & 1));
+      const int acc = kDwN128 ? 0 : (int)(jf & 1);
+      ptx::mbar_wait(&dw_full[acc], kDwN128 ? (uint32_t)(jf & 1) : (uint32_t)((jf >> 1) & 1));
       ptx::tc_fence_after();
       const int c0 = 32 * g;
       float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow) * H + c0
                          : gpart1 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow - 64) * H + c0;
       float p0[16], p1[16];
-      ptx::tmem_ld16(t_dw + 64 * acc + c0, p0);
-      ptx::tmem_ld16(t_dw + 64 * acc + c0 + 16, p1);
+      if (kDwN128) {  // columns c and 64 + c: (row block) x d_hi and x d_lo
+        float q0[16], q1[16];
+        ptx::tmem_ld16(t_dw + c0, p0);
+        ptx::tmem_ld16(t_dw + c0 + 16, p1);
+        ptx::tmem_ld16(t_dw + 64 + c0, q0);
+        ptx::tmem_ld16(t_dw + 64 + c0 + 16, q1);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          p0[j] += q0[j];
+          p1[j] += q1[j];
+        }
+      } else {
+        ptx::tmem_ld16(t_dw + 64 * acc + c0, p0);
+        ptx::tmem_ld16(t_dw + 64 * acc + c0 + 16, p1);
+      }
       float dbs = 0.f;
       if (with_db && warp < 2) {  // bias gradient: fixed-order sum of the 8 warp partials
         const float* db = dbp + (jf % 4) * 8 * 64 + trow;
@@ -377,7 +402,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     // dW MMAs of job j (which release this job's staging ring slots) can run.
     auto stage_chunk = [&](const float (&hin)[H], const float (&d)[H]) {
       if (kExp & 1) return;
-      if (job >= 2) flush(job - 2);
+      if (kDwN128 ? job >= 1 : job >= 2) flush(kDwN128 ? job - 1 : job - 2);
       const long long ts0 = PROF ? clock64() : 0;
       const int64_t gi = job * 8 + warp;  // staging chunk counter
       stage_acquire(st_empty, gi);
@@ -459,10 +484,10 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         if (EDGE) {  // d_y = de + inv_d * d_a[dst] (model.cpp:354-360)
           const float s = __ldg(a.inv_deg + row);
           const float4* da = reinterpret_cast<const float4*>(a.d_a + (int64_t)__ldg(a.dst + row) * H);
-          const float4* de = reinterpret_cast<const float4*>(a.de_io + row * H);
+          const float4* de = a.de_in ? reinterpret_cast<const float4*>(a.de_in + row * H) : nullptr;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 x1 = __ldg(da + q), x2 = ptx::ld_hint(de + q, once);  // read then rewritten in place: coherent path
+          for (int q = 0; q < 16; ++q) {  // de: read, later rewritten in place: coherent path
+            const float4 x1 = __ldg(da + q), x2 = de ? ptx::ld_hint(de + q, once) : make_float4(0.f, 0.f, 0.f, 0.f);
             dh[4 * q] = fmaf(s, x1.x, x2.x);
             dh[4 * q + 1] = fmaf(s, x1.y, x2.y);
             dh[4 * q + 2] = fmaf(s, x1.z, x2.z);
@@ -583,7 +608,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       }
       if (PROF) pf[7] += (unsigned long long)(clock64() - ti0);
     }
-    if (!(kExp & 1) && job >= 2) flush(job - 2);  // last two dW jobs of this CTA
+    if (!kDwN128 && !(kExp & 1) && job >= 2) flush(job - 2);  // last dW job(s) of this CTA
     if (!(kExp & 1) && job >= 1) flush(job - 1);
     if (PROF && warp == 0 && lane == 0) {
       pf[0] = (unsigned long long)(clock64() - pf_t0);
@@ -676,15 +701,17 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     // Separate instruction stream from the dX issuer, so the dX MMAs of one
     // slot never wait behind the other slot's staging of the current job.
     const uint32_t tm = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t*>(tmem_base_slot), 0);
-    constexpr uint32_t idesc_dw = ptx::idesc_tf32(128, H) | (1u << 15) | (1u << 16);  // A, B MN-major, N = 64
+    constexpr uint32_t idesc_dw =
+        ptx::idesc_tf32(128, kDwN128 ? 2 * H : H) | (1u << 15) | (1u << 16);  // A, B MN-major, N = 128 / 64
     int64_t gi = 0;  // staging chunk counter
     unsigned long long pc_st = 0, pc_dw = 0, pc_dwt = 0;
     const long long t_start = PROF ? clock64() : 0;
     const int64_t n_jobs = (kExp & 1) ? 0 : ((n_pairs - blockIdx.x + gridDim.x - 1) / gridDim.x) * n_dw;
     for (int64_t jd = 0; jd < n_jobs; ++jd) {
-      const int acc = (int)(jd & 1);
+      const int acc = kDwN128 ? 0 : (int)(jd & 1);
       const long long t0 = PROF ? clock64() : 0;
-      ptx::mbar_wait(&dw_empty[acc], (uint32_t)(((jd >> 1) & 1) ^ 1));  // job jd - 2 drained
+      // the accumulator's previous job (jd - 1, or jd - 2 when double-buffered) drained
+      ptx::mbar_wait(&dw_empty[acc], kDwN128 ? (uint32_t)((jd & 1) ^ 1) : (uint32_t)(((jd >> 1) & 1) ^ 1));
       ptx::tc_fence_after();
       if (PROF) pc_dw += (unsigned long long)(clock64() - t0);
       const uint32_t t_dw = ptx::opaque(tm + Cfg::DW_COL + 64 * acc);
@@ -705,7 +732,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           const uint64_t bd_hi = ad + (uint64_t)(16384 >> 4);
           const uint64_t bd_lo = bd_hi + (uint64_t)((2 * Cfg::ST_LBO) >> 4);
           ptx::mma_tf32_ss_w(t_dw, ad, bd_hi, idesc_dw, (b > 0 || ks > 0) ? 1u : 0u);
-          ptx::mma_tf32_ss_w(t_dw, ad, bd_lo, idesc_dw, 1u);
+          if (!kDwN128) ptx::mma_tf32_ss_w(t_dw, ad, bd_lo, idesc_dw, 1u);
         }
         ptx::mma_commit_w(&st_empty[((gi / Cfg::NSTAGE) & 1) * Cfg::NSTAGE + buf]);
       }

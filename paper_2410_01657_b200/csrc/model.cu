@@ -77,16 +77,16 @@ void encode(hgnn_ctx* c) {
 }
 template <int H>
 void decode(hgnn_ctx* c) {
-  gen_forward<H, 3, true, false, H>(c, c->nl, c->xs[(size_t)c->M]->p, c->y.p, c->off_dec, c->n_dec);
+  gen_forward<H, 3, true, false, H>(c, c->nl, x_buf(c, c->M), c->y.p, c->off_dec, c->n_dec);
 }
 template <int H>
 void decode_backward(hgnn_ctx* c) {
-  gen_backward<H, 3, true, false, true, H>(c, c->nl, c->xs[(size_t)c->M]->p, c->dy.p, c->dx.p, c->off_dec, c->n_dec);
+  gen_backward<H, 3, true, false, true, H>(c, c->nl, x_buf(c, c->M), c->dy.p, c->dx.p, c->off_dec, c->n_dec);
 }
 template <int H>
 void encode_backward(hgnn_ctx* c) {
   gen_backward<3, H, true, true, false, H>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
-  gen_backward<7, H, true, true, false, H>(c, c->ne, c->edge_feat.p, c->de.p, nullptr, c->off_ee, c->n_ee);
+  gen_backward<7, H, true, true, false, H>(c, c->ne, c->edge_feat.p, de_out_buf(c, 0), nullptr, c->off_ee, c->n_ee);
 }
 
 void require_model(hgnn_ctx* c) {
@@ -139,7 +139,7 @@ void model_compute_gradients(hgnn_ctx* c) {
     else decode_backward<32>(c);
   }
   // message-passing backward (model.cpp:411-415), de_M = 0 (model.cpp:412)
-  CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * H), c->stream));
+  if (!c->lean) CUDA_OK(cudaMemsetAsync(c->de.p, 0, sizeof(float) * (size_t)(c->ne * H), c->stream));
   run_backward(c);
   CUDA_OK(cudaMemcpyAsync(c->mgrads.p + c->off_mp, c->grads.p, sizeof(double) * (size_t)c->n_mp_par,
                           cudaMemcpyDeviceToDevice, c->stream));

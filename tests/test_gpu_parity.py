@@ -248,3 +248,40 @@ def test_factorized_edge_path_matches_three_segment_path(engine, E, p, H, M, k):
         assert rel(dx0, ref["dx_in"][0][0]) < BWD_TOL, fact
         assert rel(de0, ref["de_in"][0][0]) < BWD_TOL, fact
         assert grad_rel(grads, ref["grads"][0], cfg) < BWD_TOL, fact
+
+
+def test_memory_lean_plan_matches_standard(engine):
+    """The memory-lean plan (no stored last-layer e', de_m written over e_m,
+    one recomputed node-projection buffer, dx_node in place of dx, x_M in the
+    idle dY buffer — the plan that fits configs[3]'s 2-way split in 180 GB)
+    computes bitwise what the standard plan computes."""
+    from paper_2410_01657_b200 import SizeError
+    H, M, k = 64, 3, 2
+    cfg = GnnConfig("lean", H, M, k, mode="na2a")
+    g = build_rank_graph(3, 4, 1, 0, "verify")
+    mp = mp_params(cfg, init_params(cfg, 41))
+    x0, e0, dx, _ = random_inputs(g, H, 23)
+    res = {}
+    for lean in (0, 1):
+        engine.upload_graph(g)
+        engine.configure(cfg)
+        engine.upload_params(mp)
+        engine.set_option("edge_factorized", 1)
+        engine.set_option("memory_lean", lean)
+        x_out = engine.nmp_forward(x0, e0)
+        a1 = engine.trace(1, "a_sync")
+        if lean:
+            with pytest.raises(SizeError):
+                engine.trace(M - 1, "e_out")
+        res[lean] = (x_out, a1) + engine.nmp_backward(dx)
+        if lean:
+            with pytest.raises(UninitializedError):  # the backward consumed the trace storage
+                engine.trace(0, "e_in")
+    engine.set_option("memory_lean", -1)
+    engine.set_option("edge_factorized", 0)
+    for u, v in zip(res[0], res[1]):
+        assert u.tobytes() == v.tobytes()
+    ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx])
+    assert rel(res[1][0], ref["x_out"][0][M - 1]) < FWD_TOL
+    assert rel(res[1][3], ref["de_in"][0][0]) < BWD_TOL
+    assert grad_rel(res[1][4], ref["grads"][0], cfg) < BWD_TOL
