@@ -294,7 +294,7 @@ void ensure_buffers(hgnn_ctx* c) {
   if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
   if (c->ps_ready.size() != (size_t)M) c->ps_ready.assign((size_t)M, 0);
   c->fact_blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (c->rows + kFactRows - 1) / kFactRows),
-                                          (int64_t)c->num_sms * 2);
+                                          (int64_t)c->num_sms * 2);  // 112 KB shared memory: two per SM
   if (c->edge_fact && c->fact_ok && H == 64) c->fact_part.alloc((int64_t)c->fact_blocks * 2 * H * H);
   c->stage_elems = std::min<int64_t>(std::max<int64_t>(c->rows, c->ne) * H, int64_t{1} << 24);
   c->stage.alloc(std::max<int64_t>(c->stage_elems, 1));
@@ -1422,9 +1422,7 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
     CUDA_OK(cudaStreamSynchronize(c->stream));
     c->graph_ready = true;
     c->forward_done = false;
-    c->xs.clear();
-    c->es.clear();
-    c->as.clear();
+    for (auto& v : c->plan_key) v = -1;  // buffers re-planned by the next ensure_buffers
   });
 }
 
@@ -1443,9 +1441,7 @@ int hgnn_configure(hgnn_ctx* c, int64_t hidden, int64_t M, int64_t k, int mode) 
       // model level's layout (off_mp, n_full, ...) must be set up again
       c->params_ready = false;
       c->model_configured = c->model_params_ready = c->model_data_ready = false;
-      c->xs.clear();
-      c->es.clear();
-      c->as.clear();
+      for (auto& v : c->plan_key) v = -1;
     }
     c->H = hidden;
     c->M = M;

@@ -88,34 +88,67 @@ enum { kFwdProfIssTotal = 0, kFwdProfIssA = 1, kFwdProfIssW = 2, kFwdProfIssMma 
 
 __device__ __forceinline__ float elu_fast(float z) { return z > 0.f ? z : ptx::exp_fast(z) - 1.0f; }
 
-// Sum of H values with 8 independent partial sums (short dependency chains).
+// Packed fp32 (FFMA2 / FADD2 / FMUL2, sm_100): two lanes of a row per
+// instruction in the epilogue math — half the FP issue slots of the scalar code.
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2_pair(const float* v) { return make_float2(v[0], v[1]); }
+__device__ __forceinline__ void f2_put(float* v, float2 p) {
+  v[0] = p.x;
+  v[1] = p.y;
+}
+
+// Sum of H values with 8 independent partial sums (4 packed pairs, short chains).
 template <int H>
 __device__ __forceinline__ float tree_sum(const float (&v)[H]) {
-  float p[8];
+  float2 p[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) p[i] = v[i];
+  for (int i = 0; i < 4; ++i) p[i] = f2_pair(v + 2 * i);
 #pragma unroll
-  for (int j = 8; j < H; ++j) p[j % 8] += v[j];
-  return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+  for (int j = 4; j < H / 2; ++j) p[j % 4] = f2_add(p[j % 4], f2_pair(v + 2 * j));
+  const float2 q = f2_add(f2_add(p[0], p[1]), f2_add(p[2], p[3]));
+  return q.x + q.y;
 }
 
 // Parameter-free LayerNorm (kernels.cpp:81-94) with tree reductions; returns inv_std.
 template <int H>
 __device__ __forceinline__ float ln0_tree(float (&v)[H]) {
   const float mean = tree_sum<H>(v) * (1.0f / H);
-  float p[8];
+  const float2 nm = make_float2(-mean, -mean);
+  float2 p[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) p[i] = 0.f;
+  for (int i = 0; i < 4; ++i) p[i] = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < H; ++j) {
-    const float d = v[j] - mean;
-    p[j % 8] = fmaf(d, d, p[j % 8]);
+  for (int j = 0; j < H / 2; ++j) {
+    const float2 d = f2_add(f2_pair(v + 2 * j), nm);
+    p[j % 4] = f2_fma(d, d, p[j % 4]);
   }
-  const float var = (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) * (1.0f / H);
+  const float2 q = f2_add(f2_add(p[0], p[1]), f2_add(p[2], p[3]));
+  const float var = (q.x + q.y) * (1.0f / H);
   const float inv_std = ptx::rsqrt_fast(var + 1e-12f);
+  const float2 is = make_float2(inv_std, inv_std);
 #pragma unroll
-  for (int j = 0; j < H; ++j) v[j] = (v[j] - mean) * inv_std;
+  for (int j = 0; j < H / 2; ++j) f2_put(v + 2 * j, f2_mul(f2_add(f2_pair(v + 2 * j), nm), is));
   return inv_std;
+}
+
+// h += ELU(t) (kernels.cpp:263-266) on packed pairs: one FMUL2 for the
+// exponent scaling, two ex2.approx, one FADD2 for e^t - 1, selects, one FADD2.
+template <int H>
+__device__ __forceinline__ void add_elu(float (&h)[H], const float (&t)[H]) {
+  const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f), m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+  for (int j = 0; j < H / 2; ++j) {
+    const float2 tt = f2_pair(t + 2 * j);
+    const float2 z = f2_mul(tt, l2e);
+    float2 e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(z.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(z.y));
+    e = f2_add(e, m1);
+    const float2 el = make_float2(tt.x > 0.f ? tt.x : e.x, tt.y > 0.f ? tt.y : e.y);
+    f2_put(h + 2 * j, f2_add(f2_pair(h + 2 * j), el));
+  }
 }
 
 template <int H>
@@ -124,9 +157,10 @@ __device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const f
   for (int c = 0; c < H; c += 32) {
     float hi[32], lo[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < 32; j += 2) {
       hi[j] = ptx::tf32_hi(v[c + j]);
-      lo[j] = v[c + j] - hi[j];
+      hi[j + 1] = ptx::tf32_hi(v[c + j + 1]);
+      f2_put(lo + j, f2_add(f2_pair(v + c + j), make_float2(-hi[j], -hi[j + 1])));
     }
     ptx::tmem_st32(t_hi + c, hi);
     ptx::tmem_st32(t_lo + c, lo);
@@ -142,7 +176,7 @@ __device__ __forceinline__ void tc_load_d(uint32_t t_d, const float* __restrict_
     ptx::tmem_ld32(t_d + c, p);
     ptx::tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) y[c + j] = p[j] + b[c + j];
+    for (int j = 0; j < 32; j += 2) f2_put(y + c + j, f2_add(f2_pair(p + j), f2_pair(b + c + j)));
   }
 }
 
@@ -349,8 +383,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
           t0 = t1;
         }
         ln0_tree<H>(u);
-#pragma unroll
-        for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
+        add_elu<H>(h, u);
         if (PROF) {
           __syncwarp();
           e_math += (unsigned long long)(clock64() - t0);

@@ -69,6 +69,19 @@ constexpr bool kDiscardScratch = true;  // see the backward walk
 #define HGNN_DW_N128 1
 #endif
 constexpr bool kDwN128 = HGNN_DW_N128;
+// Packed fp32 (f32x2) variants of the backward epilogue pieces. Measured at C3
+// (edge backward per layer, 3 runs): all scalar 67.5 ms, all packed 69.3 ms,
+// single pieces 67.7-72.9 ms: the backward epilogue is not FP-issue bound,
+// so the scalar code (shorter, fewer register pair moves) is the default.
+#ifndef HGNN_PK_LNB
+#define HGNN_PK_LNB 0
+#endif
+#ifndef HGNN_PK_STAGE
+#define HGNN_PK_STAGE 0
+#endif
+#ifndef HGNN_PK_TMEM
+#define HGNN_PK_TMEM 0
+#endif
 #ifndef HGNN_EXP
 #define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py): bits drop work, results are wrong
 #endif
@@ -131,9 +144,15 @@ __device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const 
   for (int c = 0; c < 64; c += 16) {
     float hi[16], lo[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 16; j += 2) {
       hi[j] = ptx::tf32_hi(v[c + j]);
-      lo[j] = v[c + j] - hi[j];
+      hi[j + 1] = ptx::tf32_hi(v[c + j + 1]);
+      if (HGNN_PK_TMEM) {
+        f2_put(lo + j, f2_add(f2_pair(v + c + j), make_float2(-hi[j], -hi[j + 1])));
+      } else {
+        lo[j] = v[c + j] - hi[j];
+        lo[j + 1] = v[c + j + 1] - hi[j + 1];
+      }
     }
     ptx::tmem_st16(t_hi + c, hi);
     ptx::tmem_st16(t_lo + c, lo);
@@ -147,8 +166,16 @@ __device__ __forceinline__ void bwd_load_d(uint32_t t_d, const float* b, float (
     float p[16];
     ptx::tmem_ld16(t_d + c, p);
     ptx::tmem_wait_ld();
+    if (b && HGNN_PK_TMEM) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) y[c + j] = b ? p[j] + b[c + j] : p[j];
+      for (int j = 0; j < 16; j += 2) f2_put(y + c + j, f2_add(f2_pair(p + j), f2_pair(b + c + j)));
+    } else if (b) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) y[c + j] = p[j] + b[c + j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) y[c + j] = p[j];
+    }
   }
 }
 
@@ -205,10 +232,13 @@ __device__ __forceinline__ void stage_row(uint8_t* base, int row, const float (&
       hi.y = ptx::tf32_hi_stage(x.y);
       hi.z = ptx::tf32_hi_stage(x.z);
       hi.w = ptx::tf32_hi_stage(x.w);
-      lo.x = x.x - hi.x;
-      lo.y = x.y - hi.y;
-      lo.z = x.z - hi.z;
-      lo.w = x.w - hi.w;
+      if (HGNN_PK_STAGE) {
+        const float2 l0 = f2_add(make_float2(x.x, x.y), make_float2(-hi.x, -hi.y));
+        const float2 l1 = f2_add(make_float2(x.z, x.w), make_float2(-hi.z, -hi.w));
+        lo = make_float4(l0.x, l0.y, l1.x, l1.y);
+      } else {
+        lo = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+      }
       *reinterpret_cast<float4*>(base + st_off(q, row)) = hi;
       *reinterpret_cast<float4*>(base + st_off(16 + q, row)) = lo;
     }
@@ -474,8 +504,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         for (int q = 0; q < 16; ++q)
           st[q * 128] = make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
         scr_inv[(l - 1) * 128 + trow] = inv_std;
-#pragma unroll
-        for (int j = 0; j < H; ++j) h[j] += elu_fast(u[j]);
+        add_elu<H>(h, u);
       }
       if (PROF) pf[1] += (unsigned long long)(clock64() - tr0);
       // ---------------------------------------------- backward
@@ -523,6 +552,50 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           const float inv_std = (kExp & 2) ? 1.0f : scr_inv[(l - 1) * 128 + trow];
           const long long tl0 = PROF ? clock64() : 0;
           bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
+          if constexpr (HGNN_PK_LNB) {
+          // ELU adjoint (kernels.cpp:68-71), residual rebuild h_{l-1} = h_l - ELU(t_l),
+          // LN adjoint (kernels.cpp:99-126), on packed pairs
+          float2 p1[4], p2[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) p1[i] = p2[i] = make_float2(0.f, 0.f);
+          const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
+          const float2 m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int jx = 4 * q + 2 * u;
+              const float2 tt = u == 0 ? make_float2(t4.x, t4.y) : make_float2(t4.z, t4.w);
+              const float2 z = f2_mul(tt, l2e);
+              float2 ex;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex.x) : "f"(z.x));
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex.y) : "f"(z.y));
+              const float2 em1 = f2_add(ex, m1);
+              const float2 el = make_float2(tt.x > 0.f ? tt.x : em1.x, tt.y > 0.f ? tt.y : em1.y);
+              const float2 dp = make_float2(tt.x > 0.f ? 1.0f : ex.x, tt.y > 0.f ? 1.0f : ex.y);
+              f2_put(h + jx, f2_fma(el, m1, f2_pair(h + jx)));  // h_{l-1}
+              const float2 dd = f2_mul(f2_pair(dh + jx), dp);
+              f2_put(dh + jx, dd);
+              p1[(jx / 2) % 4] = f2_add(p1[(jx / 2) % 4], dd);
+              p2[(jx / 2) % 4] = f2_fma(dd, tt, p2[(jx / 2) % 4]);
+            }
+          }
+          const float2 s1 = f2_add(f2_add(p1[0], p1[1]), f2_add(p1[2], p1[3]));
+          const float2 s2 = f2_add(f2_add(p2[0], p2[1]), f2_add(p2[2], p2[3]));
+          const float g_mean = (s1.x + s1.y) * (1.0f / H);
+          const float gx_mean = (s2.x + s2.y) * (1.0f / H);
+          const float2 ngx = make_float2(-gx_mean, -gx_mean), ngm = make_float2(-g_mean, -g_mean);
+          const float2 is2 = make_float2(inv_std, inv_std);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
+            const float2 w0 = f2_add(f2_fma(make_float2(t4.x, t4.y), ngx, f2_pair(dh + 4 * q)), ngm);
+            const float2 w1 = f2_add(f2_fma(make_float2(t4.z, t4.w), ngx, f2_pair(dh + 4 * q + 2)), ngm);
+            f2_put(dh + 4 * q, f2_mul(w0, is2));
+            f2_put(dh + 4 * q + 2, f2_mul(w1, is2));
+          }
+          } else {
           float p1[8], p2[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
@@ -554,6 +627,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
             dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
             dh[4 * q + 3] = (dh[4 * q + 3] - g_mean - t4.w * gx_mean) * inv_std;
+          }
           }
           if (kDiscardScratch) {
             // t_l and inv_std of this tile are dead: drop their L2 lines instead

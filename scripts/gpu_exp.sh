@@ -1,4 +1,8 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py -q -x > gpurun_out/n128_pytest.log 2>&1; echo rc=$?
-timeout 600 python bench.py --steps 3 --warmup 3 --profile > gpurun_out/n128_c3.json 2>&1; echo rc=$?
-HGNN_B200_LIB=paper_2410_01657_b200/lib/exp/libhgnn_b200_expn64.so timeout 600 python bench.py --steps 3 --warmup 3 --profile > gpurun_out/n64_c3.json 2>&1; echo rc=$?
+for v in "" nolnb nostage notmem none; do
+  tag=${v:-default}
+  if [ -n "$v" ]; then export HGNN_B200_LIB=paper_2410_01657_b200/lib/exp/libhgnn_b200_exp$v.so; else unset HGNN_B200_LIB; fi
+  timeout 600 python bench.py --steps 3 --warmup 3 --profile --fact 0 > gpurun_out/pk_$tag.json 2>&1; echo rc=$?
+done
+unset HGNN_B200_LIB
+timeout 600 python bench.py --steps 3 --warmup 3 --profile --fact 1 > gpurun_out/pk_fact1.json 2>&1; echo rc=$?

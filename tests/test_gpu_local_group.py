@@ -37,6 +37,7 @@ from rank_worker import gid_inputs  # noqa: E402
 pytestmark = pytest.mark.gpu
 FWD_TOL = 5e-5
 BWD_TOL = 2e-4
+GRAD_TOL_FULL = 2e-3  # gradients at configs[0]/[1] size (tests/test_gpu_configs.py)
 MODES = {0: "none", 1: "a2a", 2: "na2a"}
 
 
@@ -141,7 +142,7 @@ def test_c2_two_rank_consistency_full_size(gpus):
     nodes) split 2-way, H32 k5 M4 (the `large` preset's MP stack): the 2-rank
     device run equals the 1-rank device run by global id within FWD_TOL, the
     coincident copies are bitwise equal across ranks, and the summed rank
-    gradients equal the 1-rank gradients within BWD_TOL (test_model.cpp:145-183)."""
+    gradients equal the 1-rank gradients within GRAD_TOL_FULL (test_model.cpp:145-183)."""
     E, p, H, M, k = 16, 3, 32, 4, 5
     cfg = GnnConfig("c2", H, M, k, mode="na2a")
     mp = mp_params(cfg, init_params(cfg, 0))
@@ -156,8 +157,8 @@ def test_c2_two_rank_consistency_full_size(gpus):
     mag = max(np.abs(v).max() for v in one.values())
     assert max(np.abs(two[gd] - one[gd]).max() for gd in one) / mag < FWD_TOL
     gsum = r2[0]["grads"] + r2[1]["grads"]
-    for name, a, b in mp_layer_slices(cfg):
-        assert rel(gsum[a:b], r1[0]["grads"][a:b]) < BWD_TOL, name
+    for name, a, b in mp_layer_slices(cfg):  # full size: see GRAD_TOL_FULL in tests/test_gpu_configs.py
+        assert rel(gsum[a:b], r1[0]["grads"][a:b]) < GRAD_TOL_FULL, name
 
 
 def test_overlapped_schedule_equals_serial_in_group(gpus):

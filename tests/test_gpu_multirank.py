@@ -147,3 +147,34 @@ def test_two_gpu_mismatched_sequence_raises(gpus):
     for r in res:
         assert bool(r["raised"]), r
         assert "mismatched collective sequence" in str(r["msg"]) or "did not complete" in str(r["msg"])
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="needs the reference compiled in place (oracle/_ref)")
+def test_c2_two_gpu_consistency(gpus):
+    """BASELINE configs[1] over NCCL: the configs[0] mesh (16^3 / P3, H32 k5 M4)
+    on 2 GPUs. Each rank matches the reference's own 2-rank run; the 2-rank
+    output equals the 1-rank reference output by gid; coincident copies are
+    bitwise equal across the GPUs (test_model.cpp:145-183, harness.cpp:147-158)."""
+    if gpus < 2:
+        pytest.skip("needs 2 GPUs")
+    E, p, H, M, k = 16, 3, 32, 4, 5
+    cfg = GnnConfig("c2", H, M, k, mode="na2a")
+    mp = mp_params(cfg, init_params(cfg, 0))
+    graphs = build_distributed_graph(E, p, 2, "verify")
+    with tempfile.TemporaryDirectory() as tmp:
+        res = launch(2, E, p, H, M, k, "na2a", tmp)
+    ins = [gid_inputs(g, H) for g in graphs]
+    ref2 = O.ref_mp_run(O.RefGraph(E, p, 2, "verify", features=False), H, M, k, "na2a", mp,
+                        [i[0] for i in ins], [i[1] for i in ins], [i[2] for i in ins])
+    for r in range(2):
+        assert rel(res[r]["x_out"], ref2.get(r, "x_out", M - 1)) < FWD_TOL
+        assert rel(res[r]["dx0"], ref2.get(r, "dx_in", 0)) < BWD_TOL
+    two, bitwise = by_gid(graphs, [res[r]["x_out"] for r in range(2)])
+    assert bitwise
+    g1 = build_distributed_graph(E, p, 1, "verify")
+    i1 = gid_inputs(g1[0], H)
+    ref1 = O.ref_mp_run(O.RefGraph(E, p, 1, "verify", features=False), H, M, k, "na2a", mp, [i1[0]], [i1[1]],
+                        [i1[2]])
+    one, _ = by_gid(g1, [ref1.get(0, "x_out", M - 1)])
+    mag = max(np.abs(v).max() for v in one.values())
+    assert max(np.abs(two[gd] - one[gd]).max() for gd in one) / mag < FWD_TOL
