@@ -73,6 +73,9 @@ constexpr bool kDwN128 = HGNN_DW_N128;
 // (edge backward per layer, 3 runs): all scalar 67.5 ms, all packed 69.3 ms,
 // single pieces 67.7-72.9 ms: the backward epilogue is not FP-issue bound,
 // so the scalar code (shorter, fewer register pair moves) is the default.
+#ifndef HGNN_PARK_AUX
+#define HGNN_PARK_AUX 1  // loader and dW-issuer waits park (mbar_wait_parked)
+#endif
 #ifndef HGNN_PK_LNB
 #define HGNN_PK_LNB 0
 #endif
@@ -785,7 +788,9 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const int acc = kDwN128 ? 0 : (int)(jd & 1);
       const long long t0 = PROF ? clock64() : 0;
       // the accumulator's previous job (jd - 1, or jd - 2 when double-buffered) drained
-      ptx::mbar_wait(&dw_empty[acc], kDwN128 ? (uint32_t)((jd & 1) ^ 1) : (uint32_t)(((jd >> 1) & 1) ^ 1));
+      const uint32_t dwe_par = kDwN128 ? (uint32_t)((jd & 1) ^ 1) : (uint32_t)(((jd >> 1) & 1) ^ 1);
+      if (HGNN_PARK_AUX) ptx::mbar_wait_parked(&dw_empty[acc], dwe_par);
+      else ptx::mbar_wait(&dw_empty[acc], dwe_par);
       ptx::tc_fence_after();
       if (PROF) pc_dw += (unsigned long long)(clock64() - t0);
       const uint32_t t_dw = ptx::opaque(tm + Cfg::DW_COL + 64 * acc);
@@ -793,7 +798,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         const int buf = (int)(gi % Cfg::NSTAGE);
         const uint32_t par = (uint32_t)((gi / Cfg::NSTAGE) & 1);
         const long long t1 = PROF ? clock64() : 0;
-        ptx::mbar_wait(&st_full[buf], par);
+        if (HGNN_PARK_AUX) ptx::mbar_wait_parked(&st_full[buf], par);
+        else ptx::mbar_wait(&st_full[buf], par);
         ptx::tc_fence_after();
         if (PROF) pc_st += (unsigned long long)(clock64() - t1);
         const uint32_t sa = ptx::smem_u32(stage + (size_t)buf * Cfg::STAGE_BYTES);
@@ -826,7 +832,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       uint32_t wph = 0;
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
         for (int j = 0; j < n_w; ++j) {
-          ptx::mbar_wait(&w_empty[ws], wph ^ 1);
+          if (HGNN_PARK_AUX) ptx::mbar_wait_parked(&w_empty[ws], wph ^ 1);
+          else ptx::mbar_wait(&w_empty[ws], wph ^ 1);
           ptx::mbar_arrive_expect_tx(&w_full[ws], Cfg::CHUNK_BYTES);
           ptx::bulk_g2s(wring + (size_t)ws * Cfg::CHUNK_FLOATS, a.chunks + (size_t)j * Cfg::CHUNK_FLOATS,
                         Cfg::CHUNK_BYTES, &w_full[ws]);

@@ -75,6 +75,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Wait for a warp off the critical path (weight loader, dW issuer): parks
+// between probes (NANOSLEEP.SYNCS), leaving the issue slots of its SM
+// sub-partition to the epilogue warps.
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_parked(bar, parity)) {
+    if (clock64() - t0 > 40000000000ll) {
+      printf("hgnn_b200: mbarrier wait timeout (block %d thread %d smem 0x%x parity %u)\n", (int)blockIdx.x,
+             (int)threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
+  }
+}
+
 // ---- bulk global -> shared copy completing on an mbarrier -----------------
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
