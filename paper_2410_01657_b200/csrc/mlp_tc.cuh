@@ -167,17 +167,14 @@ __device__ __forceinline__ void tc_store_a(uint32_t t_hi, uint32_t t_lo, const f
   }
 }
 
-// y[j] = D[:, j] + b[j]
+// y[j] = D[:, j] + b[j]; all TMEM loads in flight before the one wait
 template <int H>
 __device__ __forceinline__ void tc_load_d(uint32_t t_d, const float* __restrict__ b, float (&y)[H]) {
 #pragma unroll
-  for (int c = 0; c < H; c += 32) {
-    float p[32];
-    ptx::tmem_ld32(t_d + c, p);
-    ptx::tmem_wait_ld();
+  for (int c = 0; c < H; c += 32) ptx::tmem_ld32(t_d + c, *reinterpret_cast<float(*)[32]>(y + c));
+  ptx::tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) f2_put(y + c + j, f2_add(f2_pair(p + j), f2_pair(b + c + j)));
-  }
+  for (int j = 0; j < H; j += 2) f2_put(y + j, f2_add(f2_pair(y + j), f2_pair(b + j)));
 }
 
 __device__ __forceinline__ void tc_signal(uint64_t* bar) {
@@ -405,17 +402,11 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         ptx::mbar_wait(&y_empty[g], py ^ 1);  // previous tile of this slot consumed
         py ^= 1;
         uint8_t* yt = ytile + (size_t)g * 128 * H * 4;
+        tc_load_d<H>(t_d, bo, h);  // h is dead after the output projection's A store
 #pragma unroll
-        for (int c = 0; c < H; c += 32) {
-          float p[32];
-          ptx::tmem_ld32(t_d + c, p);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(yt + ytile_off<H>(trow, c / 4 + j)) =
-                make_float4(p[4 * j] + bo[c + 4 * j], p[4 * j + 1] + bo[c + 4 * j + 1],
-                            p[4 * j + 2] + bo[c + 4 * j + 2], p[4 * j + 3] + bo[c + 4 * j + 3]);
-        }
+        for (int j = 0; j < H / 4; ++j)
+          *reinterpret_cast<float4*>(yt + ytile_off<H>(trow, j)) =
+              make_float4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&y_full[g]);

@@ -162,13 +162,16 @@ __device__ __forceinline__ void bwd_store_a(uint32_t t_hi, uint32_t t_lo, const 
   }
 }
 
-// y = D (+ b), 16 columns at a time.
+// y = D (+ b): four 16-column TMEM loads in flight, one wait.
 __device__ __forceinline__ void bwd_load_d(uint32_t t_d, const float* b, float (&y)[64]) {
+#pragma unroll
+  for (int c = 0; c < 64; c += 16) ptx::tmem_ld16(t_d + c, *reinterpret_cast<float(*)[16]>(y + c));
+  ptx::tmem_wait_ld();
 #pragma unroll
   for (int c = 0; c < 64; c += 16) {
     float p[16];
-    ptx::tmem_ld16(t_d + c, p);
-    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) p[j] = y[c + j];
     if (b && HGNN_PK_TMEM) {
 #pragma unroll
       for (int j = 0; j < 16; j += 2) f2_put(y + c + j, f2_add(f2_pair(p + j), f2_pair(b + c + j)));
