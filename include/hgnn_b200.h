@@ -211,7 +211,7 @@ int hgnn_compute_gradients(hgnn_ctx* ctx, double* loss, double* grads, double* y
 int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double eps, double* loss);
 
 /* ---- options --------------------------------------------------------------- */
-/* "edge_factorized":  1 = (default, tcgen05 paths) the edge MLP's input linear is
+/* "edge_factorized":  1 = (tcgen05 paths; default 0) the edge MLP's input linear is
  *                     split through the nodes, P = x [W0_s | W0_d] once per node and
  *                     only e W0_e per edge; the forward edge kernel also forms the
  *                     aggregate (one fused kernel, no aggregate launch) and the
@@ -222,6 +222,13 @@ int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double
  *                     0 = SIMT fp32 kernels.
  * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
  *                      0 = SIMT fp32 kernels.
+ * "encoder_impl":      1 = (default, H = 64 with both MLP impls 1) node / edge
+ *                      encoders on the tcgen05 MLP kernels (zero-padded F-feature
+ *                      input, skip + output LayerNorm in the epilogue); 0 = SIMT.
+ * "mlp_backward_split": 1 = 16-warp split-row backward epilogue (measured slower,
+ *                      default 0).
+ * "memory_lean":       -1 = (default) auto, 0 = standard plan, 1 = lean plan.
+ * "collective_check", "collective_timeout_ms": debug collective-sequence guard. 
  * "halo_overlap":      1 = (default; R > 1, exchange mode set, tcgen05 path) forward:
  *                      boundary-row edges + aggregates first, then the exchange on
  *                      a side stream while the interior edges run; backward: the

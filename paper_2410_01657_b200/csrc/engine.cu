@@ -24,6 +24,7 @@
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
 #include "mlp_tc_bwd.cuh"
+#include "mlp_tc_bwd_cs.cuh"
 
 using namespace hgnn_b200;
 using namespace hgnn_b200::engine;
@@ -724,6 +725,14 @@ int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
   args.prof = c->prof_on ? c->prof.p + (edge ? 0 : kProfCount) : nullptr;
   const int grid = tc_bwd_grid(c, args.n_rows);
   const bool prof = args.prof != nullptr;
+  if (c->bwd_split && !prof) {  // split-row epilogue (mlp_tc_bwd_cs.cuh)
+    auto ks = mode == kEdgeFact ? mlp_tc_backward_cs_kernel<kEdgeFact>
+                                : (edge ? mlp_tc_backward_cs_kernel<kEdgeInput> : mlp_tc_backward_cs_kernel<kNodeInput>);
+    CUDA_OK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCsCfg::SMEM));
+    ks<<<grid, TcBwdCsCfg::THREADS, TcBwdCsCfg::SMEM, c->stream>>>(args);
+    check_launch(c);
+    return grid;
+  }
   auto k = mode == kEdgeFact
                ? (prof ? mlp_tc_backward_kernel<kEdgeFact, true> : mlp_tc_backward_kernel<kEdgeFact, false>)
                : edge ? (prof ? mlp_tc_backward_kernel<kEdgeInput, true> : mlp_tc_backward_kernel<kEdgeInput, false>)
@@ -1667,6 +1676,9 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value < -1 || value > 1) fail(HGNN_ERR_CONFIG, "memory_lean: -1 (auto), 0 or 1");
       c->lean_opt = (int)value;
       for (auto& v : c->plan_key) v = -1;  // re-plan at the next call
+    } else if (k == "mlp_backward_split") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_split: 0 or 1");
+      c->bwd_split = (int)value;
     } else if (k == "collective_check") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "collective_check: 0 or 1");
       c->coll_check = (int)value;
@@ -1674,6 +1686,9 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value <= 0) fail(HGNN_ERR_CONFIG, "collective_timeout_ms must be positive");
       c->coll_timeout_ms = value;
       if (c->group) c->group->timeout_ms = value;
+    } else if (k == "encoder_impl") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "encoder_impl: 0 (simt) or 1 (tcgen05, H = 64)");
+      c->enc_impl = (int)value;
     } else if (k == "mlp_backward_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_impl: 0 (simt) or 1 (tcgen05)");
       c->bwd_impl = (int)value;

@@ -118,6 +118,7 @@ struct hgnn_ctx {
   hgnn_b200::DevBuf<double> grads;
   int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
   int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
+  int bwd_split = 0;                    // option "mlp_backward_split": 16-warp split-row epilogue (measured slower, off)
   hgnn_b200::DevBuf<float> bchunks;                // backward chunk sequence per MLP
   std::vector<int64_t> bchunk_off;
   hgnn_b200::DevBuf<float> tc_scratch;
@@ -173,6 +174,14 @@ struct hgnn_ctx {
   hgnn_b200::DevBuf<double> loss_part, loss_st;               // block partials; [s, n, seed]
   hgnn_b200::DevBuf<int32_t> pt_src;                          // par_t[i] = par[pt_src[i]] (MP block)
   hgnn_b200::DevBuf<uint32_t> ch_map, bch_map;                // chunk refresh maps (bit 31: tf32 lo part)
+  // tcgen05 encoders (option "encoder_impl", H = 64): forward / backward chunk
+  // sequences of the node and edge encoder MLPs (zero-padded F-feature input
+  // segment), refreshed from the fp64 master through enc_map ([fwd | bwd])
+  int enc_impl = 1;
+  hgnn_b200::DevBuf<float> enc_ch;
+  hgnn_b200::DevBuf<uint32_t> enc_map;                        // 0x7fffffff: zero padding
+  int64_t enc_off[4] = {0, 0, 0, 0};                          // fwd node, fwd edge, bwd node, bwd edge
+  hgnn_b200::DevBuf<float> enc_tmp, enc_part;                 // pre-LN output / its adjoint; LN-adjoint partials
   hgnn_b200::DevBuf<int> nonfinite;
   int64_t adam_step = 0;
   double last_loss = 0.0;
@@ -234,7 +243,8 @@ void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int s
       for (int kk = 0; kk < H; ++kk)
         for (int n = 0; n < H; ++n) {
           const int cidx = l == 0 ? seg0 + ci : 0;
-          const int64_t src = w + (int64_t)(cidx * H + kk) * H + n;
+          const int r = cidx * H + kk;  // row of W_l (W0 rows >= in_dim: zero padding, src -1)
+          const int64_t src = (l == 0 && r >= in_dim) ? -1 : w + (int64_t)r * H + n;
           emit(base + tc_chunk_index(n, kk, H), src, false);
           emit(base + tc_chunk_index(H + n, kk, H), src, true);
         }
@@ -257,10 +267,13 @@ void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int s
     base += 2 * (int64_t)H * H;
   };
   auto W = [&](int l) { return mlp_w_offset(l, in_dim, H); };
-  for (int c = seg0; c < seg0 + nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + kk) * H + n; });
+  // W0 rows >= in_dim are zero padding (src -1): the encoders' F-feature input
+  for (int c = seg0; c < seg0 + nseg; ++c)
+    chunk([&](int n, int kk) { return c * H + kk < in_dim ? W(0) + (int64_t)(c * H + kk) * H + n : (int64_t)-1; });
   for (int l = 1; l <= K; ++l) chunk([&](int n, int kk) { return W(l) + (int64_t)kk * H + n; });
   for (int l = K + 1; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * H + kk; });
-  for (int c = seg0; c < seg0 + nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * H + n) * H + kk; });
+  for (int c = seg0; c < seg0 + nseg; ++c)
+    chunk([&](int n, int kk) { return c * H + n < in_dim ? W(0) + (int64_t)(c * H + n) * H + kk : (int64_t)-1; });
 }
 inline int64_t chunk_floats_fwd(int in_dim, int H, int K, int nseg = -1) {
   return (int64_t)((nseg < 0 ? in_dim / H : nseg) + K + 1) * 2 * H * H;

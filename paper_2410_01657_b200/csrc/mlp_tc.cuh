@@ -52,6 +52,7 @@ struct TcCfg {
   static constexpr size_t OFF_Y = OFF_BIAS + 18 * H * 4;              // kEdgeFact: 2 output tiles (128 x H)
   static constexpr size_t SMEM = OFF_Y + 1024;                         // + biases (k <= 16)
   static constexpr size_t SMEM_FACT = OFF_Y + 2 * 128 * H * 4 + 1024;
+  static constexpr size_t SMEM_ENC = OFF_Y + 10 * H * 4 + 1024;       // kEncoder: skip W (<= 8 x H), LN gamma, beta
 };
 
 // Index (in floats) of B element (n, k) inside a chunk (K-major core matrices).
@@ -78,6 +79,13 @@ struct TcFwdArgs {
   const float* proj;     // rows x 2H: [P_s | P_d] = x [W0_s | W0_d]
   const float* inv;      // per slot 1/d
   float* agg;            // rows x H aggregate (rows with an empty segment are not written)
+  // kEncoder (encoder MLP, model.cpp:70-80): e_in = n_rows x in_dim features
+  // (in_dim <= 8, zero-padded to one K = H segment); params in the encoder's
+  // for_each layout (GenLayout, mlp_generic.cuh); out = LN(y) * gamma + beta
+  // with y = MLP(x) + x W_skip, or y itself (enc_ln = 0: the backward's
+  // pre-LayerNorm recompute)
+  int in_dim;
+  int enc_ln;
 };
 
 // Optional instrumentation of the forward kernel (cycles summed over CTAs;
@@ -186,6 +194,17 @@ __device__ __forceinline__ void tc_signal(uint64_t* bar) {
 
 template <int H, int MODE>
 __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool valid, int c, float (&v)[H]) {
+  if (MODE == kEncoder) {  // in_dim (<= 8) features, zero-padded to H
+#pragma unroll
+    for (int j = 0; j < H; ++j) v[j] = 0.f;
+    if (valid) {
+      const float* f = a.e_in + row * a.in_dim;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < a.in_dim) v[j] = __ldg(f + j);
+    }
+    return;
+  }
   if (valid) {
     const float* seg;
     if (MODE == kEdgeFact)
@@ -242,8 +261,10 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   using Cfg = TcCfg<H>;
   constexpr bool FACT = MODE == kEdgeFact;
   constexpr bool FUSED = MODE == kEdgeFact || MODE == kEdgeFused;  // segment tiles + in-kernel aggregate
-  constexpr int nseg = MODE == kEdgeFact ? 1 : (MODE == kNodeInput ? 2 : 3);
-  constexpr int in_dim = (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout (kEdgeFact: the 3H-input MLP)
+  constexpr bool ENC = MODE == kEncoder;
+  constexpr int nseg = (MODE == kEdgeFact || ENC) ? 1 : (MODE == kNodeInput ? 2 : 3);
+  // parameter layout (kEdgeFact: the 3H-input MLP; kEncoder: F input features)
+  const int in_dim = ENC ? a.in_dim : (MODE == kNodeInput ? 2 : 3) * H;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* wring = reinterpret_cast<float*>(smem);
@@ -258,6 +279,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(y_empty + 2);
   float* sbias = reinterpret_cast<float*>(smem + Cfg::OFF_BIAS);  // (k+2) x H
   uint8_t* ytile = smem + Cfg::OFF_Y;                             // kEdgeFact: [2][128][H] swizzled
+  float* senc = reinterpret_cast<float*>(smem + Cfg::OFF_Y);       // kEncoder: W_skip [8][H], gamma, beta
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -291,6 +313,16 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   }
   for (int i = threadIdx.x; i < (a.k + 2) * H; i += blockDim.x)
     sbias[i] = __ldg(a.params + mlp_b_offset(i / H, in_dim, H) + (i % H));
+  if (ENC) {  // GenLayout{in_dim, H, k, H}: skip at b(k+1) + H, then gamma, beta
+    const int64_t skip = mlp_b_offset(a.k + 1, in_dim, H) + H;
+    for (int i = threadIdx.x; i < 10 * H; i += blockDim.x) {
+      const int r = i / H;
+      float w = 0.f;
+      if (r < in_dim) w = __ldg(a.params + skip + i);
+      else if (r >= 8) w = __ldg(a.params + skip + (int64_t)in_dim * H + (r - 8) * H + (i % H));
+      senc[i] = w;
+    }
+  }
   if (warp == 8) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_base_slot);
   ptx::tc_fence_before();
   __syncthreads();
@@ -410,6 +442,33 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&y_full[g]);
+      } else if (ENC) {  // y = D + b + x W_skip, output LayerNorm (mlp_generic.cuh forward)
+        float xf[8];
+        {
+          const float* f = a.e_in + row * a.in_dim;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xf[i] = (valid && i < a.in_dim) ? __ldg(f + i) : 0.f;
+        }
+        tc_load_d<H>(t_d, sbias + (a.k + 1) * H, h);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < a.in_dim) {
+#pragma unroll
+            for (int j = 0; j < H; j += 2)
+              f2_put(h + j, f2_fma(make_float2(xf[i], xf[i]), f2_pair(senc + i * H + j), f2_pair(h + j)));
+          }
+        }
+        if (a.enc_ln) {
+          ln0_tree<H>(h);
+#pragma unroll
+          for (int j = 0; j < H; j += 2)
+            f2_put(h + j, f2_fma(f2_pair(h + j), f2_pair(senc + 8 * H + j), f2_pair(senc + 9 * H + j)));
+        }
+        if (valid) {
+          float4* o = reinterpret_cast<float4*>(a.out + row * H);
+#pragma unroll
+          for (int j = 0; j < H / 4; ++j) o[j] = make_float4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+        }
       } else {  // stream y = D + b straight to global, 32 columns at a time
         const float* bo = sbias + (a.k + 1) * H;
         float4* o = reinterpret_cast<float4*>(a.out + row * H);

@@ -115,6 +115,12 @@ struct TcBwdArgs {
   float* scratch;        // [gridDim.x][2][k][16][128] float4 + [gridDim.x][2][k][128] inv_std
   int k;
   unsigned long long* prof;  // optional: wait-cycle counters (see kProf*)
+  // kEncoder: in_dim input features (<= 8, zero-padded to one segment; the
+  // padded rows of dW0 are not written, no input adjoint is stored), d_out =
+  // adjoint of the pre-LayerNorm output (enc_out_backward_kernel), n_par =
+  // stride of the gradient partials (the encoder's full parameter count)
+  int in_dim;
+  int64_t n_par;
 };
 
 // Optional instrumentation of the MMA issuer (cycles, summed over CTAs).
@@ -131,6 +137,7 @@ __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool
   f.x = a.x;
   f.e_in = a.e_in;
   f.a = a.a;
+  f.in_dim = a.in_dim;
   tc_gather<64, MODE>(f, row, valid, c, v);
 }
 __device__ __forceinline__ void bwd_gather_proj(const TcBwdArgs& a, int64_t row, bool valid, float (&v)[64]) {
@@ -289,9 +296,10 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   using Cfg = TcBwdCfg;
   constexpr int H = Cfg::H;
   constexpr bool FACT = MODE == kEdgeFact;
-  constexpr bool EDGE = MODE != kNodeInput;
+  constexpr bool ENC = MODE == kEncoder;
+  constexpr bool EDGE = MODE != kNodeInput && !ENC;
   constexpr int nseg = MODE == kEdgeInput ? 3 : (MODE == kNodeInput ? 2 : 1);
-  constexpr int in_dim = (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout
+  const int in_dim = ENC ? a.in_dim : (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout
   constexpr int seg0 = FACT ? 2 : 0;                         // W0 row block of the first input segment
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   const int n_dw = K + 1 + nseg;            // dW jobs per pair
   const int64_t n_tiles = (a.n_rows + 127) / 128;
   const int64_t n_pairs = (n_tiles + 1) / 2;
-  const int64_t n_par = mlp_param_count(in_dim, H, K);
+  const int64_t n_par = ENC ? a.n_par : mlp_param_count(in_dim, H, K);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::WSTAGES; ++s) {
@@ -394,6 +402,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const int c0 = 32 * g;
       float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow) * H + c0
                          : gpart1 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow - 64) * H + c0;
+      // kEncoder: rows >= in_dim of dW0 belong to the zero padding
+      const bool w_ok = !ENC || lin > 0 || (wq < 2 ? trow : trow - 64) < in_dim;
       float p0[16], p1[16];
       if (kDwN128) {  // columns c and 64 + c: (row block) x d_hi and x d_lo
         float q0[16], q1[16];
@@ -424,10 +434,12 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       // Fire-and-forget vector reductions into this CTA's partial: every
       // element has a single owning thread, so the adds land in program order
       // (deterministic) and no load latency is exposed.
+      if (w_ok) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        ptx::red_add4_hint(gw + 4 * j, p0[4 * j], p0[4 * j + 1], p0[4 * j + 2], p0[4 * j + 3], keep);
-        ptx::red_add4_hint(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3], keep);
+        for (int j = 0; j < 4; ++j) {
+          ptx::red_add4_hint(gw + 4 * j, p0[4 * j], p0[4 * j + 1], p0[4 * j + 2], p0[4 * j + 3], keep);
+          ptx::red_add4_hint(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3], keep);
+        }
       }
       if (with_db && warp < 2)
         asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(dbs)
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           else outp = c == 0 ? a.d_a_out : a.d_x_out;
           float4* o = reinterpret_cast<float4*>(outp + row * H);
 #pragma unroll
-          for (int cc = 0; cc < H; cc += 16) {
+          for (int cc = 0; cc < (ENC ? 0 : H); cc += 16) {  // kEncoder: the feature adjoint is not needed
             float p[16];
             ptx::tmem_ld16(t_d + cc, p);
             ptx::tmem_wait_ld();

@@ -3,8 +3,10 @@
 // 390-424, 455-579; nn.cpp:331-360) and their C-ABI (include/hgnn_b200.h).
 #include <cmath>
 
+#include "encoder_tc.cuh"
 #include "engine_ctx.hpp"
 #include "mlp_generic.cuh"
+#include "mlp_tc_bwd.cuh"
 #include "model_kernels.cuh"
 
 using namespace hgnn_b200;
@@ -68,10 +70,134 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
   check_launch(c);
 }
 
+// ---- tcgen05 encoders (encoder_tc.cuh) ------------------------------------
+bool enc_tc(const hgnn_ctx* c) { return c->enc_impl == 1 && c->H == 64 && c->fwd_impl == 1 && c->bwd_impl == 1; }
+
+// which: 0 node encoder, 1 edge encoder. enc_ln = 0: pre-LayerNorm y (backward recompute).
+void enc_forward_tc(hgnn_ctx* c, int which, int64_t n, int F, const float* feat, float* out, int64_t par_off,
+                    int enc_ln) {
+  if (n == 0) return;
+  using Cfg = TcCfg<64>;
+  TcFwdArgs a{};
+  a.n_rows = n;
+  a.e_in = feat;
+  a.out = out;
+  a.chunks = c->enc_ch.p + c->enc_off[which];
+  a.params = c->gen_par.p + par_off;
+  a.k = (int)c->K;
+  a.in_dim = F;
+  a.enc_ln = enc_ln;
+  auto k = mlp_tc_forward_kernel<64, kEncoder, false>;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_ENC));
+  const int64_t pairs = ((n + 127) / 128 + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM_ENC, c->stream>>>(a);
+  check_launch(c);
+}
+
+// A device buffer of >= n floats that is dead while the encoder backward runs:
+// d_x_src (or x_M under the memory-lean plan), else a dedicated one.
+float* enc_scratch(hgnn_ctx* c, int64_t n) {
+  if (c->dsrc.n >= n) return c->dsrc.p;
+  if (c->enc_tmp.n < n) c->enc_tmp.alloc(n);
+  return c->enc_tmp.p;
+}
+
+// Parameter gradients of one encoder into mgrads[par_off, par_off + n_par)
+// (rank-local); d_out = adjoint of the encoder output (N x 64).
+void enc_backward_tc(hgnn_ctx* c, int which, int64_t n, int F, const float* feat, const float* d_out,
+                     int64_t par_off, int64_t n_par) {
+  if (n == 0) {
+    CUDA_OK(cudaMemsetAsync(c->mgrads.p + par_off, 0, sizeof(double) * (size_t)n_par, c->stream));
+    return;
+  }
+  constexpr int H = 64;
+  const int K = (int)c->K;
+  const GenLayout L{F, H, K, H};
+  float* y = enc_scratch(c, n * H);
+  enc_forward_tc(c, which, n, F, feat, y, par_off, 0);  // 1. pre-LayerNorm y
+  const int n_ln = (F + 2) * H;                          // 2. LN adjoint in place, W_skip / gamma / beta partials
+  if (c->enc_part.n < (int64_t)kEncLnBlocks * n_ln) c->enc_part.alloc((int64_t)kEncLnBlocks * n_ln);
+  enc_out_backward_kernel<<<kEncLnBlocks, kEncLnThreads, 0, c->stream>>>(y, d_out, feat, F,
+                                                                        c->gen_par.p + par_off + L.ln_g(), n,
+                                                                        c->enc_part.p);
+  check_launch(c);
+  // 3. the MLP backward on the tensor cores, d_out = dy
+  const int64_t pairs = ((n + 127) / 128 + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  if (c->grad_part.n < 2 * (int64_t)grid * n_par) c->grad_part.alloc(2 * (int64_t)grid * n_par);
+  CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * grid * n_par), c->stream));
+  TcBwdArgs a{};
+  a.n_rows = n;
+  a.e_in = feat;
+  a.d_out = y;
+  a.chunks = c->enc_ch.p + c->enc_off[2 + which];
+  a.params = c->gen_par.p + par_off;
+  a.grad_partial = c->grad_part.p;
+  a.scratch = c->tc_scratch.p;
+  a.k = K;
+  a.in_dim = F;
+  a.n_par = n_par;
+  auto k = mlp_tc_backward_kernel<kEncoder, false>;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
+  k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(a);
+  check_launch(c);
+  // W, b partials (the skip / LayerNorm entries of these partials stay zero) ...
+  reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->grad_part.p, 2 * grid, n_par,
+                                                                          c->mgrads.p + par_off);
+  check_launch(c);
+  // ... then W_skip, gamma, beta (contiguous in the for_each layout)
+  reduce_partials_kernel<<<blocks_for(n_ln), kEwThreads, 0, c->stream>>>(c->enc_part.p, kEncLnBlocks, n_ln,
+                                                                         c->mgrads.p + par_off + L.skip());
+  check_launch(c);
+}
+
+// Encoder chunk sequences (fwd node, fwd edge, bwd node, bwd edge) as a
+// refresh map over the full fp64 parameter vector.
+void build_enc_map(hgnn_ctx* c) {
+  const int H = (int)c->H, K = (int)c->K;
+  if (H != 64) {
+    c->enc_map.release();
+    c->enc_ch.release();
+    return;
+  }
+  const int Fs[2] = {(int)c->fx, (int)c->fe};
+  const int64_t offs[2] = {c->off_ne, c->off_ee};
+  int64_t total = 0;
+  for (int d = 0; d < 2; ++d)
+    for (int w = 0; w < 2; ++w) {
+      c->enc_off[2 * d + w] = total;
+      total += d == 0 ? chunk_floats_fwd(Fs[w], H, K, 1) : chunk_floats_bwd(Fs[w], H, K, 1);
+    }
+  std::vector<uint32_t> map((size_t)total);
+  for (int d = 0; d < 2; ++d)
+    for (int w = 0; w < 2; ++w) {
+      auto emit = [&](int64_t pos, int64_t src, bool lo) {
+        map[(size_t)pos] = src < 0 ? 0x7fffffffu : ((uint32_t)(offs[w] + src) | (lo ? 0x80000000u : 0u));
+      };
+      if (d == 0) chunk_layout_fwd(Fs[w], H, K, c->enc_off[2 * d + w], emit, 0, 1);
+      else chunk_layout_bwd(Fs[w], H, K, c->enc_off[2 * d + w], emit, 0, 1);
+    }
+  c->enc_map.upload(map.data(), total, c->stream);
+  c->enc_ch.alloc(total);
+}
+
+void refresh_enc_chunks(hgnn_ctx* c) {
+  if (c->enc_map.n == 0) return;
+  chunk_refresh_kernel<<<blocks_for(c->enc_map.n), kEwThreads, 0, c->stream>>>(c->mparams.p, c->enc_map.p,
+                                                                              c->enc_map.n, c->enc_ch.p);
+  check_launch(c);
+}
+
 // Encoders / decoder of width H (model.cpp:70-101): node encoder F_x = 3,
 // edge encoder F_e = 7, decoder F_y = 3.
 template <int H>
 void encode(hgnn_ctx* c) {
+  if (H == 64 && enc_tc(c)) {
+    enc_forward_tc(c, 0, c->rows, (int)c->fx, c->node_feat.p, c->xs[0]->p, c->off_ne, 1);
+    enc_forward_tc(c, 1, c->ne, (int)c->fe, c->edge_feat.p, c->es[0]->p, c->off_ee, 1);
+    return;
+  }
   gen_forward<3, H, true, true, H>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
   gen_forward<7, H, true, true, H>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
 }
@@ -85,6 +211,11 @@ void decode_backward(hgnn_ctx* c) {
 }
 template <int H>
 void encode_backward(hgnn_ctx* c) {
+  if (H == 64 && enc_tc(c)) {
+    enc_backward_tc(c, 0, c->rows, (int)c->fx, c->node_feat.p, c->dx.p, c->off_ne, c->n_ne);
+    enc_backward_tc(c, 1, c->ne, (int)c->fe, c->edge_feat.p, de_out_buf(c, 0), c->off_ee, c->n_ee);
+    return;
+  }
   gen_backward<3, H, true, true, false, H>(c, c->rows, c->node_feat.p, c->dx.p, nullptr, c->off_ne, c->n_ne);
   gen_backward<7, H, true, true, false, H>(c, c->ne, c->edge_feat.p, de_out_buf(c, 0), nullptr, c->off_ee, c->n_ee);
 }
@@ -181,6 +312,7 @@ void model_refresh_params(hgnn_ctx* c) {
                                                                                 c->bchunks.p);
     check_launch(c);
   }
+  refresh_enc_chunks(c);
 }
 
 // Device-refresh maps of the MP block (same element placement as the host
@@ -218,6 +350,8 @@ void build_refresh_maps(hgnn_ctx* c) {
   c->pt_src.upload(pt.data(), (int64_t)pt.size(), c->stream);
   c->ch_map.upload(ch.data(), (int64_t)ch.size(), c->stream);
   c->bch_map.upload(bch.data(), (int64_t)bch.size(), c->stream);
+  build_enc_map(c);
+  refresh_enc_chunks(c);
 }
 
 

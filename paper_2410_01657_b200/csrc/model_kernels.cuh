@@ -132,6 +132,10 @@ __global__ void chunk_refresh_kernel(const double* __restrict__ src, const uint3
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t m = map[i];
+  if (m == 0x7fffffffu) {  // zero padding (the encoders' F-feature input segment)
+    dst[i] = 0.f;
+    return;
+  }
   const float w = (float)src[m & 0x7fffffffu];
   const float hi = tf32_rna_bits(w);
   dst[i] = (m >> 31) ? tf32_rna_bits(w - hi) : hi;

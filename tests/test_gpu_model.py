@@ -52,7 +52,7 @@ def engine(gpus):
     eng.close()
 
 
-@pytest.mark.parametrize("E,p,M,k", [(2, 3, 2, 2), (3, 2, 1, 5)])
+@pytest.mark.parametrize("E,p,M,k", [(2, 3, 2, 2), (3, 2, 1, 5), (6, 3, 2, 5)])
 def test_compute_gradients_matches_reference(engine, E, p, M, k):
     H, seed = 64, 3
     cfg, ref_g, _ = setup(engine, E, p, H, M, k, seed)
@@ -62,6 +62,25 @@ def test_compute_gradients_matches_reference(engine, E, p, M, k):
     assert rel(y, ref.get(0, "y")) < LOSS_TOL
     ref_grads = ref.get(0, "all_grads")
     worst = max((rel(grads[a:b], ref_grads[a:b]), name) for name, a, b in model_slices(cfg))
+    assert worst[0] < BWD_TOL, worst
+
+
+@pytest.mark.parametrize("E,p,M,k", [(3, 2, 1, 5), (6, 3, 2, 3)])
+def test_tensor_core_encoders_match_simt(gpus, E, p, M, k):
+    """encoder_impl 1 (tcgen05 encoders, encoder_tc.cuh) against 0 (fp32
+    SIMT, mlp_generic.cuh) on the same inputs: loss, output and every
+    gradient tensor (incl. the encoders' W_skip / LayerNorm gamma, beta)."""
+    out = {}
+    for impl in (0, 1):
+        eng = Engine(0)
+        eng.set_option("encoder_impl", impl)
+        cfg, _, _ = setup(eng, E, p, 64, M, k, 11)
+        out[impl] = eng.compute_gradients()
+        eng.close()
+    (l0, g0, y0), (l1, g1, y1) = out[0], out[1]
+    assert abs(l1 - l0) / abs(l0) < LOSS_TOL, (l0, l1)
+    assert rel(y1, y0) < LOSS_TOL
+    worst = max((rel(g1[a:b], g0[a:b]), name) for name, a, b in model_slices(cfg))
     assert worst[0] < BWD_TOL, worst
 
 
