@@ -1,5 +1,5 @@
-// Encoders on the tensor cores (sm_100a, H = 64; SURVEY §8f row 1,
-// model.cpp:70-80): the node / edge encoder MLP
+// Encoders and decoder on the tensor cores (sm_100a, H = 64; SURVEY §8f row 1,
+// model.cpp:70-101). The node / edge encoder MLP
 //   h = x W0 + b0;  h += ELU(LN0(h Wj + bj)), j = 1..k;
 //   y = h W_{k+1} + b_{k+1} + x W_skip;  out = LN(y) * gamma + beta
 // runs through the processor-MLP tcgen05 kernels in mode kEncoder: the F
@@ -12,6 +12,10 @@
 //      of y, and forms the gamma / beta / W_skip gradient partials,
 //   3. the tcgen05 backward kernel (mlp_tc_bwd.cuh, kEncoder) walks the MLP
 //      with d_out = dy: dW_{k+1} .. dW0 (padded rows dropped), the biases.
+// The decoder (y = MLP(x_M) + x_M W_skip, F_y <= 8 outputs, no LayerNorm) is
+// mode kDecoder: the output linear's columns >= F_y are zero padding, the
+// forward epilogue adds the skip product; its backward is the tcgen05 kernel
+// (input adjoint of the MLP) plus dec_skip_backward_kernel (skip adjoint, W_skip).
 #pragma once
 
 #include <cstdint>
@@ -94,6 +98,63 @@ __global__ void __launch_bounds__(kEncLnThreads) enc_out_backward_kernel(float* 
   r[(F + 1) * H + c0 + 1] = db[1];
   __syncthreads();
   const int n_out = (F + 2) * H;
+  for (int j = threadIdx.x; j < n_out; j += kEncLnThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < kEncLnThreads / 32; ++w) s += red[w][j];
+    part[(int64_t)blockIdx.x * n_out + j] = s;
+  }
+}
+
+// Decoder skip term (model.cpp:92-101) around the tcgen05 decoder MLP
+// (kDecoder): dx += dy W_skip^T on the MLP's input adjoint, and the W_skip
+// gradient partials part[block][H x F] (= sum x^T dy; fixed warp / row
+// assignment and warp order: deterministic). x, dx: n x 64, dy: n x F (<= 8),
+// wskip: 64 x F.
+__global__ void __launch_bounds__(kEncLnThreads) dec_skip_backward_kernel(const float* __restrict__ x,
+                                                                          const float* __restrict__ dy,
+                                                                          const float* __restrict__ wskip, int F,
+                                                                          int64_t n, float* __restrict__ dx,
+                                                                          float* __restrict__ part) {
+  constexpr int H = 64;
+  __shared__ float red[kEncLnThreads / 32][8 * H];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c0 = 2 * lane;
+  float w0[8], w1[8], acc0[8], acc1[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    w0[o] = o < F ? __ldg(wskip + c0 * F + o) : 0.f;
+    w1[o] = o < F ? __ldg(wskip + (c0 + 1) * F + o) : 0.f;
+    acc0[o] = acc1[o] = 0.f;
+  }
+  const int64_t n_warps = (int64_t)gridDim.x * (kEncLnThreads / 32);
+  for (int64_t row = (int64_t)blockIdx.x * (kEncLnThreads / 32) + warp; row < n; row += n_warps) {
+    const float dl = lane < F ? __ldg(dy + row * F + lane) : 0.f;
+    const float2 xv = __ldg(reinterpret_cast<const float2*>(x + row * H) + lane);
+    float2* dr = reinterpret_cast<float2*>(dx + row * H) + lane;
+    float2 dv = *dr;
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      if (o < F) {
+        const float d = __shfl_sync(0xffffffffu, dl, o);
+        dv.x = fmaf(d, w0[o], dv.x);
+        dv.y = fmaf(d, w1[o], dv.y);
+        acc0[o] = fmaf(xv.x, d, acc0[o]);
+        acc1[o] = fmaf(xv.y, d, acc1[o]);
+      }
+    }
+    *dr = dv;
+  }
+  float* r = red[warp];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    if (o < F) {
+      r[c0 * F + o] = acc0[o];
+      r[(c0 + 1) * F + o] = acc1[o];
+    }
+  }
+  __syncthreads();
+  const int n_out = H * F;
   for (int j = threadIdx.x; j < n_out; j += kEncLnThreads) {
     float s = 0.f;
 #pragma unroll

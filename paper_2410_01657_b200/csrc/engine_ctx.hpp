@@ -180,7 +180,7 @@ struct hgnn_ctx {
   int enc_impl = 1;
   hgnn_b200::DevBuf<float> enc_ch;
   hgnn_b200::DevBuf<uint32_t> enc_map;                        // 0x7fffffff: zero padding
-  int64_t enc_off[4] = {0, 0, 0, 0};                          // fwd node, fwd edge, bwd node, bwd edge
+  int64_t enc_off[6] = {0, 0, 0, 0, 0, 0};                    // fwd node, edge, decoder; bwd node, edge, decoder
   hgnn_b200::DevBuf<float> enc_tmp, enc_part;                 // pre-LN output / its adjoint; LN-adjoint partials
   hgnn_b200::DevBuf<int> nonfinite;
   int64_t adam_step = 0;
@@ -233,9 +233,13 @@ struct Timed {
 // seg0 / nseg: the input segments (K = H row blocks of W0) the kernel
 // multiplies on the tensor cores: all of them, or only the e block (seg0 = 2,
 // nseg = 1) for the factorised edge MLP (kEdgeFact).
+// out_dim < H (the decoder): W_{k+1} is H x out_dim, its columns >= out_dim
+// are zero padding (src -1).
 template <class Emit>
-void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int seg0 = 0, int nseg = -1) {
+void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int seg0 = 0, int nseg = -1,
+                      int out_dim = -1) {
   if (nseg < 0) nseg = in_dim / H;
+  if (out_dim < 0) out_dim = H;
   for (int l = 0; l < K + 2; ++l) {
     const int64_t w = mlp_w_offset(l, in_dim, H);
     const int n_ch = l == 0 ? nseg : 1;
@@ -244,7 +248,8 @@ void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int s
         for (int n = 0; n < H; ++n) {
           const int cidx = l == 0 ? seg0 + ci : 0;
           const int r = cidx * H + kk;  // row of W_l (W0 rows >= in_dim: zero padding, src -1)
-          const int64_t src = (l == 0 && r >= in_dim) ? -1 : w + (int64_t)r * H + n;
+          int64_t src = (l == 0 && r >= in_dim) ? -1 : w + (int64_t)r * H + n;
+          if (l == K + 1 && out_dim < H) src = n < out_dim ? w + (int64_t)kk * out_dim + n : -1;
           emit(base + tc_chunk_index(n, kk, H), src, false);
           emit(base + tc_chunk_index(H + n, kk, H), src, true);
         }
@@ -255,8 +260,10 @@ void chunk_layout_fwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int s
 // per input segment. A transposed chunk stores element (n = input feature,
 // k = output feature) = W[n][k].
 template <class Emit>
-void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int seg0 = 0, int nseg = -1) {
+void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int seg0 = 0, int nseg = -1,
+                      int out_dim = -1) {
   if (nseg < 0) nseg = in_dim / H;
+  if (out_dim < 0) out_dim = H;
   auto chunk = [&](auto src_of) {
     for (int kk = 0; kk < H; ++kk)
       for (int n = 0; n < H; ++n) {
@@ -271,7 +278,8 @@ void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int s
   for (int c = seg0; c < seg0 + nseg; ++c)
     chunk([&](int n, int kk) { return c * H + kk < in_dim ? W(0) + (int64_t)(c * H + kk) * H + n : (int64_t)-1; });
   for (int l = 1; l <= K; ++l) chunk([&](int n, int kk) { return W(l) + (int64_t)kk * H + n; });
-  for (int l = K + 1; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * H + kk; });
+  chunk([&](int n, int kk) { return kk < out_dim ? W(K + 1) + (int64_t)n * out_dim + kk : (int64_t)-1; });
+  for (int l = K; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * H + kk; });
   for (int c = seg0; c < seg0 + nseg; ++c)
     chunk([&](int n, int kk) { return c * H + n < in_dim ? W(0) + (int64_t)(c * H + n) * H + kk : (int64_t)-1; });
 }

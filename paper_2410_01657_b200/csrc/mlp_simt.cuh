@@ -27,7 +27,7 @@ constexpr int kColStride = kMlpThreads + kColPad;
 // computed once per node (tensor-core kernels only; same parameters).
 // kEdgeFused: kEdgeInput's 3-segment input with the aggregate formed in the
 // same kernel (tensor-core forward only).
-enum MlpInput : int { kEdgeInput = 0, kNodeInput = 1, kEdgeFact = 2, kEdgeFused = 3, kEncoder = 4 };
+enum MlpInput : int { kEdgeInput = 0, kNodeInput = 1, kEdgeFact = 2, kEdgeFused = 3, kEncoder = 4, kDecoder = 5 };
 
 // Flattened processor-MLP parameters (for_each order, fp32): W0 (in x H), b0,
 // W1, b1, ..., W_{k+1}, b_{k+1}. wt points at the same list with every W

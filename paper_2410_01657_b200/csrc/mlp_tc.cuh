@@ -86,6 +86,10 @@ struct TcFwdArgs {
   // pre-LayerNorm recompute)
   int in_dim;
   int enc_ln;
+  // kDecoder (decoder MLP, model.cpp:92-101): x rows (H wide) in, out =
+  // n_rows x out_dim (<= 8): y = MLP(x) + x W_skip, the output linear's
+  // columns >= out_dim zero-padded in the chunks
+  int out_dim;
 };
 
 // Optional instrumentation of the forward kernel (cycles summed over CTAs;
@@ -209,6 +213,8 @@ __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool 
     const float* seg;
     if (MODE == kEdgeFact)
       seg = a.e_in + row * H;
+    else if (MODE == kDecoder)
+      seg = a.x + row * H;
     else if (MODE == kEdgeInput || MODE == kEdgeFused)
       seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * H
                    : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
@@ -262,9 +268,10 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   constexpr bool FACT = MODE == kEdgeFact;
   constexpr bool FUSED = MODE == kEdgeFact || MODE == kEdgeFused;  // segment tiles + in-kernel aggregate
   constexpr bool ENC = MODE == kEncoder;
-  constexpr int nseg = (MODE == kEdgeFact || ENC) ? 1 : (MODE == kNodeInput ? 2 : 3);
+  constexpr bool DEC = MODE == kDecoder;
+  constexpr int nseg = (MODE == kEdgeFact || ENC || DEC) ? 1 : (MODE == kNodeInput ? 2 : 3);
   // parameter layout (kEdgeFact: the 3H-input MLP; kEncoder: F input features)
-  const int in_dim = ENC ? a.in_dim : (MODE == kNodeInput ? 2 : 3) * H;
+  const int in_dim = ENC ? a.in_dim : (DEC ? H : (MODE == kNodeInput ? 2 : 3) * H);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* wring = reinterpret_cast<float*>(smem);
@@ -311,8 +318,20 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     }
     ptx::fence_mbarrier_init();
   }
-  for (int i = threadIdx.x; i < (a.k + 2) * H; i += blockDim.x)
-    sbias[i] = __ldg(a.params + mlp_b_offset(i / H, in_dim, H) + (i % H));
+  for (int i = threadIdx.x; i < (a.k + 2) * H; i += blockDim.x) {
+    const int l = i / H, j = i % H;
+    if (DEC && l == a.k + 1)  // decoder output bias: out_dim entries after W_{k+1} (H x out_dim)
+      sbias[i] = j < a.out_dim ? __ldg(a.params + mlp_w_offset(l, H, H) + H * a.out_dim + j) : 0.f;
+    else
+      sbias[i] = __ldg(a.params + mlp_b_offset(l, in_dim, H) + j);
+  }
+  if (DEC) {  // W_skip (H x out_dim) as [H][8]
+    const int64_t skip = mlp_w_offset(a.k + 1, H, H) + (H + 1) * a.out_dim;
+    for (int i = threadIdx.x; i < 8 * H; i += blockDim.x) {
+      const int r = i / 8, o = i % 8;
+      senc[i] = o < a.out_dim ? __ldg(a.params + skip + r * a.out_dim + o) : 0.f;
+    }
+  }
   if (ENC) {  // GenLayout{in_dim, H, k, H}: skip at b(k+1) + H, then gamma, beta
     const int64_t skip = mlp_b_offset(a.k + 1, in_dim, H) + H;
     for (int i = threadIdx.x; i < 10 * H; i += blockDim.x) {
@@ -442,6 +461,28 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&y_full[g]);
+      } else if (DEC) {  // y = D + b + x W_skip on the first out_dim columns
+        float p[16];
+        ptx::tmem_ld16(t_d, p);
+        ptx::tmem_wait_ld();
+        float y[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) y[o] = p[o] + sbias[(a.k + 1) * H + o];
+        if (valid) {
+          const float4* xr = reinterpret_cast<const float4*>(a.x + row * H);
+#pragma unroll 4
+          for (int q = 0; q < H / 4; ++q) {
+            const float4 xv = __ldg(xr + q);
+            const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int o = 0; o < 8; ++o) y[o] = fmaf(xs[u], senc[(4 * q + u) * 8 + o], y[o]);
+          }
+#pragma unroll
+          for (int o = 0; o < 8; ++o)
+            if (o < a.out_dim) a.out[row * a.out_dim + o] = y[o];
+        }
       } else if (ENC) {  // y = D + b + x W_skip, output LayerNorm (mlp_generic.cuh forward)
         float xf[8];
         {

@@ -121,6 +121,10 @@ struct TcBwdArgs {
   // stride of the gradient partials (the encoder's full parameter count)
   int in_dim;
   int64_t n_par;
+  // kDecoder: x = decoder input rows (H wide), d_out = n_rows x out_dim output
+  // adjoint (zero-padded to H), d_x_out = the MLP part of the input adjoint;
+  // W_{k+1} is H x out_dim in the gradient layout
+  int out_dim;
 };
 
 // Optional instrumentation of the MMA issuer (cycles, summed over CTAs).
@@ -138,6 +142,7 @@ __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool
   f.e_in = a.e_in;
   f.a = a.a;
   f.in_dim = a.in_dim;
+  f.out_dim = a.out_dim;
   tc_gather<64, MODE>(f, row, valid, c, v);
 }
 __device__ __forceinline__ void bwd_gather_proj(const TcBwdArgs& a, int64_t row, bool valid, float (&v)[64]) {
@@ -297,9 +302,10 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   constexpr int H = Cfg::H;
   constexpr bool FACT = MODE == kEdgeFact;
   constexpr bool ENC = MODE == kEncoder;
-  constexpr bool EDGE = MODE != kNodeInput && !ENC;
+  constexpr bool DEC = MODE == kDecoder;
+  constexpr bool EDGE = MODE != kNodeInput && !ENC && !DEC;
   constexpr int nseg = MODE == kEdgeInput ? 3 : (MODE == kNodeInput ? 2 : 1);
-  const int in_dim = ENC ? a.in_dim : (MODE == kNodeInput ? 2 : 3) * H;  // parameter layout
+  const int in_dim = ENC ? a.in_dim : (DEC ? H : (MODE == kNodeInput ? 2 : 3) * H);  // parameter layout
   constexpr int seg0 = FACT ? 2 : 0;                         // W0 row block of the first input segment
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   const int n_dw = K + 1 + nseg;            // dW jobs per pair
   const int64_t n_tiles = (a.n_rows + 127) / 128;
   const int64_t n_pairs = (n_tiles + 1) / 2;
-  const int64_t n_par = ENC ? a.n_par : mlp_param_count(in_dim, H, K);
+  const int64_t n_par = (ENC || DEC) ? a.n_par : mlp_param_count(in_dim, H, K);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::WSTAGES; ++s) {
@@ -350,7 +356,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
     }
     ptx::fence_mbarrier_init();
   }
-  for (int i = threadIdx.x; i < (K + 2) * H; i += blockDim.x)
+  // biases of the recomputed linears 0..K (the output bias has no backward use)
+  for (int i = threadIdx.x; i < (K + 1) * H; i += blockDim.x)
     sbias[i] = __ldg(a.params + mlp_b_offset(i / H, in_dim, H) + (i % H));
   if (warp == 8) ptx::tmem_alloc<512>(tmem_base_slot);
   ptx::tc_fence_before();
@@ -402,8 +409,9 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const int c0 = 32 * g;
       float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow) * H + c0
                          : gpart1 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow - 64) * H + c0;
-      // kEncoder: rows >= in_dim of dW0 belong to the zero padding
-      const bool w_ok = !ENC || lin > 0 || (wq < 2 ? trow : trow - 64) < in_dim;
+      // kEncoder: rows >= in_dim of dW0 belong to the zero padding; kDecoder:
+      // dW_{k+1} is H x out_dim (columns >= out_dim are padding)
+      const bool w_ok = (!ENC || lin > 0 || (wq < 2 ? trow : trow - 64) < in_dim) && !(DEC && lin == K + 1);
       float p0[16], p1[16];
       if (kDwN128) {  // columns c and 64 + c: (row block) x d_hi and x d_lo
         float q0[16], q1[16];
@@ -441,9 +449,20 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           ptx::red_add4_hint(gw + 16 + 4 * j, p1[4 * j], p1[4 * j + 1], p1[4 * j + 2], p1[4 * j + 3], keep);
         }
       }
-      if (with_db && warp < 2)
+      if (DEC && lin == K + 1) {
+        const int64_t wk = mlp_w_offset(K + 1, H, H);
+        float* gd = (wq < 2 ? gpart0 + wk + (int64_t)trow * a.out_dim : gpart1 + wk + (int64_t)(trow - 64) * a.out_dim);
+        if (g == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < a.out_dim) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gd + j), "f"(p0[j]) : "memory");
+        }
+        if (warp == 0 && trow < a.out_dim)
+          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + wk + H * a.out_dim + trow), "f"(dbs) : "memory");
+      } else if (with_db && warp < 2) {
         asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(dbs)
                      : "memory");
+      }
       if (PROF) pf[2] += (unsigned long long)(clock64() - tf0);
     };
     // Job j - 2 shares this job's accumulator and must be drained before the
@@ -540,6 +559,12 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             dh[4 * q + 2] = fmaf(s, x1.z, x2.z);
             dh[4 * q + 3] = fmaf(s, x1.w, x2.w);
           }
+        } else if (DEC) {
+#pragma unroll
+          for (int j = 0; j < H; ++j) dh[j] = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < a.out_dim) dh[j] = __ldg(a.d_out + row * a.out_dim + j);
         } else {
           const float4* dy = reinterpret_cast<const float4*>(a.d_out + row * H);
 #pragma unroll
@@ -681,6 +706,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           float* outp;
           if (FACT) outp = a.de_io;
           else if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
+          else if (DEC) outp = a.d_x_out;
           else outp = c == 0 ? a.d_a_out : a.d_x_out;
           float4* o = reinterpret_cast<float4*>(outp + row * H);
 #pragma unroll

@@ -66,7 +66,7 @@ void gen_backward(hgnn_ctx* c, int64_t n_rows, const float* in, const float* d_o
   k<<<grid, kGenThreads, smem, c->stream>>>(a);
   check_launch(c);
   reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->gen_part.p, grid, n_par,
-                                                                          c->mgrads.p + par_off);
+                                                                          c->mgrads.p + par_off, n_par);
   check_launch(c);
 }
 
@@ -125,35 +125,37 @@ void enc_backward_tc(hgnn_ctx* c, int which, int64_t n, int F, const float* feat
   // 3. the MLP backward on the tensor cores, d_out = dy
   const int64_t pairs = ((n + 127) / 128 + 1) / 2;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
-  if (c->grad_part.n < 2 * (int64_t)grid * n_par) c->grad_part.alloc(2 * (int64_t)grid * n_par);
-  CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * grid * n_par), c->stream));
+  const int64_t stride = (n_par + 3) & ~int64_t(3);  // 16-byte aligned partial rows (vector reductions)
+  if (c->grad_part.n < 2 * (int64_t)grid * stride) c->grad_part.alloc(2 * (int64_t)grid * stride);
+  CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * grid * stride), c->stream));
   TcBwdArgs a{};
   a.n_rows = n;
   a.e_in = feat;
   a.d_out = y;
-  a.chunks = c->enc_ch.p + c->enc_off[2 + which];
+  a.chunks = c->enc_ch.p + c->enc_off[3 + which];
   a.params = c->gen_par.p + par_off;
   a.grad_partial = c->grad_part.p;
   a.scratch = c->tc_scratch.p;
   a.k = K;
   a.in_dim = F;
-  a.n_par = n_par;
+  a.n_par = stride;
   auto k = mlp_tc_backward_kernel<kEncoder, false>;
   CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
   k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(a);
   check_launch(c);
   // W, b partials (the skip / LayerNorm entries of these partials stay zero) ...
   reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->grad_part.p, 2 * grid, n_par,
-                                                                          c->mgrads.p + par_off);
+                                                                          c->mgrads.p + par_off, stride);
   check_launch(c);
   // ... then W_skip, gamma, beta (contiguous in the for_each layout)
   reduce_partials_kernel<<<blocks_for(n_ln), kEwThreads, 0, c->stream>>>(c->enc_part.p, kEncLnBlocks, n_ln,
-                                                                         c->mgrads.p + par_off + L.skip());
+                                                                         c->mgrads.p + par_off + L.skip(), n_ln);
   check_launch(c);
 }
 
-// Encoder chunk sequences (fwd node, fwd edge, bwd node, bwd edge) as a
-// refresh map over the full fp64 parameter vector.
+// Chunk sequences of the node encoder, edge encoder and decoder (fwd at
+// enc_off[0..2], bwd at enc_off[3..5]) as a refresh map over the full fp64
+// parameter vector.
 void build_enc_map(hgnn_ctx* c) {
   const int H = (int)c->H, K = (int)c->K;
   if (H != 64) {
@@ -161,22 +163,23 @@ void build_enc_map(hgnn_ctx* c) {
     c->enc_ch.release();
     return;
   }
-  const int Fs[2] = {(int)c->fx, (int)c->fe};
-  const int64_t offs[2] = {c->off_ne, c->off_ee};
+  const int Fs[3] = {(int)c->fx, (int)c->fe, H};   // input widths
+  const int Os[3] = {H, H, (int)c->fy};             // output widths
+  const int64_t offs[3] = {c->off_ne, c->off_ee, c->off_dec};
   int64_t total = 0;
   for (int d = 0; d < 2; ++d)
-    for (int w = 0; w < 2; ++w) {
-      c->enc_off[2 * d + w] = total;
+    for (int w = 0; w < 3; ++w) {
+      c->enc_off[3 * d + w] = total;
       total += d == 0 ? chunk_floats_fwd(Fs[w], H, K, 1) : chunk_floats_bwd(Fs[w], H, K, 1);
     }
   std::vector<uint32_t> map((size_t)total);
   for (int d = 0; d < 2; ++d)
-    for (int w = 0; w < 2; ++w) {
+    for (int w = 0; w < 3; ++w) {
       auto emit = [&](int64_t pos, int64_t src, bool lo) {
         map[(size_t)pos] = src < 0 ? 0x7fffffffu : ((uint32_t)(offs[w] + src) | (lo ? 0x80000000u : 0u));
       };
-      if (d == 0) chunk_layout_fwd(Fs[w], H, K, c->enc_off[2 * d + w], emit, 0, 1);
-      else chunk_layout_bwd(Fs[w], H, K, c->enc_off[2 * d + w], emit, 0, 1);
+      if (d == 0) chunk_layout_fwd(Fs[w], H, K, c->enc_off[3 * d + w], emit, 0, 1, Os[w]);
+      else chunk_layout_bwd(Fs[w], H, K, c->enc_off[3 * d + w], emit, 0, 1, Os[w]);
     }
   c->enc_map.upload(map.data(), total, c->stream);
   c->enc_ch.alloc(total);
@@ -201,12 +204,88 @@ void encode(hgnn_ctx* c) {
   gen_forward<3, H, true, true, H>(c, c->rows, c->node_feat.p, c->xs[0]->p, c->off_ne, c->n_ne);
   gen_forward<7, H, true, true, H>(c, c->ne, c->edge_feat.p, c->es[0]->p, c->off_ee, c->n_ee);
 }
+// decoder (kDecoder): y = MLP(x_M) + x_M W_skip on the local rows
+void dec_forward_tc(hgnn_ctx* c) {
+  if (c->nl == 0) return;
+  using Cfg = TcCfg<64>;
+  TcFwdArgs a{};
+  a.n_rows = c->nl;
+  a.x = x_buf(c, c->M);
+  a.out = c->y.p;
+  a.chunks = c->enc_ch.p + c->enc_off[2];
+  a.params = c->gen_par.p + c->off_dec;
+  a.k = (int)c->K;
+  a.in_dim = (int)c->H;
+  a.out_dim = (int)c->fy;
+  auto k = mlp_tc_forward_kernel<64, kDecoder, false>;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_ENC));
+  const int64_t pairs = ((c->nl + 127) / 128 + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM_ENC, c->stream>>>(a);
+  check_launch(c);
+}
+
+// decoder backward: dx (zeroed by the caller) = the input adjoint on the local
+// rows, gradients into mgrads[off_dec, off_dec + n_dec)
+void dec_backward_tc(hgnn_ctx* c) {
+  const int64_t n = c->nl, n_par = c->n_dec;
+  if (n == 0) {
+    CUDA_OK(cudaMemsetAsync(c->mgrads.p + c->off_dec, 0, sizeof(double) * (size_t)n_par, c->stream));
+    return;
+  }
+  constexpr int H = 64;
+  const int K = (int)c->K, F = (int)c->fy;
+  const GenLayout L{H, F, K, H};
+  const int64_t pairs = ((n + 127) / 128 + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms));
+  const int64_t stride = (n_par + 3) & ~int64_t(3);  // 16-byte aligned partial rows (vector reductions)
+  if (c->grad_part.n < 2 * (int64_t)grid * stride) c->grad_part.alloc(2 * (int64_t)grid * stride);
+  CUDA_OK(cudaMemsetAsync(c->grad_part.p, 0, sizeof(float) * (size_t)(2 * grid * stride), c->stream));
+  const float* x = x_buf(c, c->M);
+  TcBwdArgs a{};
+  a.n_rows = n;
+  a.x = x;
+  a.d_out = c->dy.p;
+  a.d_x_out = c->dx.p;
+  a.chunks = c->enc_ch.p + c->enc_off[5];
+  a.params = c->gen_par.p + c->off_dec;
+  a.grad_partial = c->grad_part.p;
+  a.scratch = c->tc_scratch.p;
+  a.k = K;
+  a.in_dim = H;
+  a.out_dim = F;
+  a.n_par = stride;
+  auto k = mlp_tc_backward_kernel<kDecoder, false>;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
+  k<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(a);
+  check_launch(c);
+  reduce_partials_kernel<<<blocks_for(n_par), kEwThreads, 0, c->stream>>>(c->grad_part.p, 2 * grid, n_par,
+                                                                          c->mgrads.p + c->off_dec, stride);
+  check_launch(c);
+  const int n_sk = H * F;
+  if (c->enc_part.n < (int64_t)kEncLnBlocks * n_sk) c->enc_part.alloc((int64_t)kEncLnBlocks * n_sk);
+  dec_skip_backward_kernel<<<kEncLnBlocks, kEncLnThreads, 0, c->stream>>>(
+      x, c->dy.p, c->gen_par.p + c->off_dec + L.skip(), F, n, c->dx.p, c->enc_part.p);
+  check_launch(c);
+  reduce_partials_kernel<<<blocks_for(n_sk), kEwThreads, 0, c->stream>>>(c->enc_part.p, kEncLnBlocks, n_sk,
+                                                                         c->mgrads.p + c->off_dec + L.skip(), n_sk);
+  check_launch(c);
+}
+
 template <int H>
 void decode(hgnn_ctx* c) {
+  if (H == 64 && enc_tc(c)) {
+    dec_forward_tc(c);
+    return;
+  }
   gen_forward<H, 3, true, false, H>(c, c->nl, x_buf(c, c->M), c->y.p, c->off_dec, c->n_dec);
 }
 template <int H>
 void decode_backward(hgnn_ctx* c) {
+  if (H == 64 && enc_tc(c)) {
+    dec_backward_tc(c);
+    return;
+  }
   gen_backward<H, 3, true, false, true, H>(c, c->nl, x_buf(c, c->M), c->dy.p, c->dx.p, c->off_dec, c->n_dec);
 }
 template <int H>

@@ -77,13 +77,13 @@ __global__ void scale_f64_kernel(double* __restrict__ v, int64_t n, double s) {
   if (i < n) v[i] *= s;
 }
 
-// fp32 partials [blocks][n] -> dst[n] (fp64), fixed block order
+// fp32 partials [blocks][stride] -> dst[n] (fp64, n <= stride), fixed block order
 __global__ void reduce_partials_kernel(const float* __restrict__ part, int64_t blocks, int64_t n,
-                                       double* __restrict__ dst) {
+                                       double* __restrict__ dst, int64_t stride) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
-  for (int64_t b = 0; b < blocks; ++b) s += (double)part[b * n + i];
+  for (int64_t b = 0; b < blocks; ++b) s += (double)part[b * stride + i];
   dst[i] = s;
 }
 

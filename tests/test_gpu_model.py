@@ -67,9 +67,9 @@ def test_compute_gradients_matches_reference(engine, E, p, M, k):
 
 @pytest.mark.parametrize("E,p,M,k", [(3, 2, 1, 5), (6, 3, 2, 3)])
 def test_tensor_core_encoders_match_simt(gpus, E, p, M, k):
-    """encoder_impl 1 (tcgen05 encoders, encoder_tc.cuh) against 0 (fp32
+    """encoder_impl 1 (tcgen05 encoders and decoder, encoder_tc.cuh) against 0 (fp32
     SIMT, mlp_generic.cuh) on the same inputs: loss, output and every
-    gradient tensor (incl. the encoders' W_skip / LayerNorm gamma, beta)."""
+    gradient tensor (incl. W_skip and the encoders' LayerNorm gamma, beta)."""
     out = {}
     for impl in (0, 1):
         eng = Engine(0)
