@@ -196,8 +196,13 @@ __device__ __forceinline__ void tc_signal(uint64_t* bar) {
   if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar);
 }
 
+#ifndef HGNN_EXP
+#define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py); bit 32: forward input gathers dropped
+#endif
+
 template <int H, int MODE>
 __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool valid, int c, float (&v)[H]) {
+  if (HGNN_EXP & 32) valid = false;
   if (MODE == kEncoder) {  // in_dim (<= 8) features, zero-padded to H
 #pragma unroll
     for (int j = 0; j < H; ++j) v[j] = 0.f;
@@ -220,13 +225,21 @@ __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool 
                    : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * H : a.e_in + row * H);
     else
       seg = c == 0 ? a.a + row * H : a.x + row * H;
+#ifndef HGNN_LDG256
+#define HGNN_LDG256 1
+#endif
+    if (HGNN_LDG256) {
 #pragma unroll
-    for (int j = 0; j < H / 4; ++j) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(seg) + j);
-      v[4 * j] = t.x;
-      v[4 * j + 1] = t.y;
-      v[4 * j + 2] = t.z;
-      v[4 * j + 3] = t.w;
+      for (int j = 0; j < H / 8; ++j) ptx::ldg256(seg + 8 * j, v + 8 * j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < H / 4; ++j) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(seg) + j);
+        v[4 * j] = t.x;
+        v[4 * j + 1] = t.y;
+        v[4 * j + 2] = t.z;
+        v[4 * j + 3] = t.w;
+      }
     }
   } else {
 #pragma unroll
@@ -242,15 +255,15 @@ __device__ __forceinline__ void tc_gather_proj(const TcFwdArgs& a, int64_t row, 
     for (int j = 0; j < H; ++j) v[j] = 0.f;
     return;
   }
-  const float4* ps = reinterpret_cast<const float4*>(a.proj + (int64_t)__ldg(a.src + row) * (2 * H));
-  const float4* pd = reinterpret_cast<const float4*>(a.proj + (int64_t)__ldg(a.dst + row) * (2 * H) + H);
+  const float* ps = a.proj + (int64_t)__ldg(a.src + row) * (2 * H);
+  const float* pd = a.proj + (int64_t)__ldg(a.dst + row) * (2 * H) + H;
 #pragma unroll
-  for (int j = 0; j < H / 4; ++j) {
-    const float4 s = __ldg(ps + j), d = __ldg(pd + j);
-    v[4 * j] = s.x + d.x;
-    v[4 * j + 1] = s.y + d.y;
-    v[4 * j + 2] = s.z + d.z;
-    v[4 * j + 3] = s.w + d.w;
+  for (int j = 0; j < H / 8; ++j) {
+    float s[8], d[8];
+    ptx::ldg256(ps + 8 * j, s);
+    ptx::ldg256(pd + 8 * j, d);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[8 * j + i] = s[i] + d[i];
   }
 }
 
@@ -506,13 +519,11 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
             f2_put(h + j, f2_fma(f2_pair(h + j), f2_pair(senc + 8 * H + j), f2_pair(senc + 9 * H + j)));
         }
         if (valid) {
-          float4* o = reinterpret_cast<float4*>(a.out + row * H);
 #pragma unroll
-          for (int j = 0; j < H / 4; ++j) o[j] = make_float4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+          for (int j = 0; j < H / 8; ++j) ptx::stg256(a.out + row * H + 8 * j, h + 8 * j);
         }
       } else {  // stream y = D + b straight to global, 32 columns at a time
         const float* bo = sbias + (a.k + 1) * H;
-        float4* o = reinterpret_cast<float4*>(a.out + row * H);
 #pragma unroll
         for (int c = 0; c < H; c += 32) {
           float p[32];
@@ -520,9 +531,9 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
           ptx::tmem_wait_ld();
           if (valid) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              o[c / 4 + j] = make_float4(p[4 * j] + bo[c + 4 * j], p[4 * j + 1] + bo[c + 4 * j + 1],
-                                         p[4 * j + 2] + bo[c + 4 * j + 2], p[4 * j + 3] + bo[c + 4 * j + 3]);
+            for (int j = 0; j < 32; ++j) p[j] += bo[c + j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ptx::stg256(a.out + row * H + c + 8 * j, p + 8 * j);
           }
         }
       }

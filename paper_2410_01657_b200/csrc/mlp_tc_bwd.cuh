@@ -85,6 +85,9 @@ constexpr bool kDwN128 = HGNN_DW_N128;
 #ifndef HGNN_PK_TMEM
 #define HGNN_PK_TMEM 0
 #endif
+#ifndef HGNN_BWD_PREFETCH
+#define HGNN_BWD_PREFETCH 0  // 1: input-segment gathers one step ahead (behind the MMA / dX wait): measured neutral at C3 (edge 67.4 ms, node 9.85 vs 9.5 ms)
+#endif
 #ifndef HGNN_EXP
 #define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py): bits drop work, results are wrong
 #endif
@@ -498,22 +501,26 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       if (PROF) pf[5] += (unsigned long long)(clock64() - t0);
     };
 
+    float h[H];
+    bool h_ready = false;  // h holds this tile's input segment 0 (gathered during the previous tile)
     for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
       const int64_t row = (2 * pair + g) * 128 + trow;
       const bool valid = row < a.n_rows;
-      float h[H];
       const long long tr0 = PROF ? clock64() : 0;
       // ---------------------------------------------- forward recompute
+      // (segment c + 1 is gathered while the MMA of segment c runs)
+      if (!HGNN_BWD_PREFETCH || !h_ready) bwd_gather<MODE>(a, row, valid, 0, h);
 #pragma unroll 1
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
           ptx::mbar_wait(&a_empty[g], pe);
           pe ^= 1;
           ptx::tc_fence_after();
+          if (!HGNN_BWD_PREFETCH) bwd_gather<MODE>(a, row, valid, c, h);
         }
-        bwd_gather<MODE>(a, row, valid, c, h);
         bwd_store_a(t_ahi, t_alo, h);
         tc_signal(&a_full[g]);
+        if (HGNN_BWD_PREFETCH && c + 1 < nseg) bwd_gather<MODE>(a, row, valid, c + 1, h);
       }
       if (FACT) bwd_gather_proj(a, row, valid, h);  // P_s[src] + P_d[dst], during the e W0_e MMA
       ptx::mbar_wait(&d_full[g], pd);
@@ -549,15 +556,20 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       if (valid) {
         if (EDGE) {  // d_y = de + inv_d * d_a[dst] (model.cpp:354-360)
           const float s = __ldg(a.inv_deg + row);
-          const float4* da = reinterpret_cast<const float4*>(a.d_a + (int64_t)__ldg(a.dst + row) * H);
+          const float* da = a.d_a + (int64_t)__ldg(a.dst + row) * H;
           const float4* de = a.de_in ? reinterpret_cast<const float4*>(a.de_in + row * H) : nullptr;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {  // de: read, later rewritten in place: coherent path
-            const float4 x1 = __ldg(da + q), x2 = de ? ptx::ld_hint(de + q, once) : make_float4(0.f, 0.f, 0.f, 0.f);
-            dh[4 * q] = fmaf(s, x1.x, x2.x);
-            dh[4 * q + 1] = fmaf(s, x1.y, x2.y);
-            dh[4 * q + 2] = fmaf(s, x1.z, x2.z);
-            dh[4 * q + 3] = fmaf(s, x1.w, x2.w);
+          for (int q = 0; q < 8; ++q) {  // de: read, later rewritten in place: coherent path
+            float x1[8];
+            ptx::ldg256(da + 8 * q, x1);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const float4 x2 = de ? ptx::ld_hint(de + 2 * q + u, once) : make_float4(0.f, 0.f, 0.f, 0.f);
+              dh[8 * q + 4 * u] = fmaf(s, x1[4 * u], x2.x);
+              dh[8 * q + 4 * u + 1] = fmaf(s, x1[4 * u + 1], x2.y);
+              dh[8 * q + 4 * u + 2] = fmaf(s, x1[4 * u + 2], x2.z);
+              dh[8 * q + 4 * u + 3] = fmaf(s, x1[4 * u + 3], x2.w);
+            }
           }
         } else if (DEC) {
 #pragma unroll
@@ -566,15 +578,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           for (int j = 0; j < 8; ++j)
             if (j < a.out_dim) dh[j] = __ldg(a.d_out + row * a.out_dim + j);
         } else {
-          const float4* dy = reinterpret_cast<const float4*>(a.d_out + row * H);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 x1 = __ldg(dy + q);
-            dh[4 * q] = x1.x;
-            dh[4 * q + 1] = x1.y;
-            dh[4 * q + 2] = x1.z;
-            dh[4 * q + 3] = x1.w;
-          }
+          for (int q = 0; q < 8; ++q) ptx::ldg256(a.d_out + row * H + 8 * q, dh + 8 * q);
         }
       } else {
 #pragma unroll
@@ -691,13 +696,20 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           write_db(dh);
         }
         if (FACT && c == 0 && valid) {  // dY: the input linear's output adjoint, for the node-level sums
-          float4* o = reinterpret_cast<float4*>(a.dy_out + row * H);
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            ptx::st_hint(o + q, make_float4(dh[4 * q], dh[4 * q + 1], dh[4 * q + 2], dh[4 * q + 3]), once);
+          for (int q = 0; q < 8; ++q) ptx::stg256_hint(a.dy_out + row * H + 8 * q, dh + 8 * q, once);
         }
-        if (c >= 0) bwd_gather<MODE>(a, row, valid, c, h);  // dW0 segment operand
+        if (c >= 0 && !HGNN_BWD_PREFETCH) bwd_gather<MODE>(a, row, valid, c, h);  // dW0 segment operand
         stage_chunk(h, dh);
+        if (HGNN_BWD_PREFETCH && jb >= K) {  // h is dead: fetch the next dW0 segment operand, or the next
+          if (c + 1 < nseg) {                // tile's first input segment, behind the dX wait
+            bwd_gather<MODE>(a, row, valid, c + 1, h);
+          } else {
+            const int64_t nrow = (2 * (pair + gridDim.x) + g) * 128 + trow;
+            h_ready = pair + gridDim.x < n_pairs;
+            if (h_ready) bwd_gather<MODE>(a, nrow, nrow < a.n_rows, 0, h);
+          }
+        }
         wait_dx();
         ++job;
         if (c < 0) {
@@ -708,17 +720,14 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           else if (MODE == kEdgeInput) outp = c == 0 ? a.d_src : (c == 1 ? a.d_dst : a.de_io);
           else if (DEC) outp = a.d_x_out;
           else outp = c == 0 ? a.d_a_out : a.d_x_out;
-          float4* o = reinterpret_cast<float4*>(outp + row * H);
 #pragma unroll
           for (int cc = 0; cc < (ENC ? 0 : H); cc += 16) {  // kEncoder: the feature adjoint is not needed
             float p[16];
             ptx::tmem_ld16(t_d + cc, p);
             ptx::tmem_wait_ld();
             if (valid) {
-#pragma unroll
-              for (int jx = 0; jx < 4; ++jx)
-                ptx::st_hint(o + cc / 4 + jx, make_float4(p[4 * jx], p[4 * jx + 1], p[4 * jx + 2], p[4 * jx + 3]),
-                             once);
+              ptx::stg256_hint(outp + row * H + cc, p, once);
+              ptx::stg256_hint(outp + row * H + cc + 8, p + 8, once);
             }
           }
           if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays

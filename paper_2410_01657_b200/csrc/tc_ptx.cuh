@@ -322,6 +322,23 @@ __device__ __forceinline__ float4 ld_hint(const float4* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
+// 32 bytes (8 floats) per thread in one 256-bit load (LDG.256, sm_100): half
+// the load instructions / L1 wavefronts of two 128-bit loads for row gathers
+__device__ __forceinline__ void ldg256(const float* p, float* v) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void stg256(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void stg256_hint(float* p, const float* v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "l"(pol)
+               : "memory");
+}
 // read-only stream (non-coherent path, no L1 allocation)
 __device__ __forceinline__ float4 ld_stream(const float4* p, uint64_t pol) {
   float4 v;

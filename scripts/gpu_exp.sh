@@ -1,3 +1,7 @@
+# timing ablations (lib/exp builds from scripts/build_exp.py; results wrong by construction)
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "tensor_core_backward or engine_matches_oracle or factorized or lean or deterministic" > gpurun_out/cs_pytest.log 2>&1; echo rc=$?
-timeout 600 python bench.py --steps 3 --warmup 3 --profile > gpurun_out/cs_c3.json 2>&1; echo rc=$?
+for v in "" 32 48; do
+  tag=${v:-default}
+  if [ -n "$v" ]; then export HGNN_B200_LIB=paper_2410_01657_b200/lib/exp/libhgnn_b200_exp$v.so; else unset HGNN_B200_LIB; fi
+  timeout 600 python bench.py --steps 3 --warmup 3 --profile > gpurun_out/ab_$tag.json 2>&1; echo rc=$?
+done
