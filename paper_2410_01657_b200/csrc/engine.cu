@@ -292,7 +292,7 @@ void ensure_buffers(hgnn_ctx* c) {
   c->grad_part.alloc(2 * (max_grid + c->num_sms) * max_par);
   const int64_t n_slots = (2 * c->K + 1) * H + c->K;
   c->scratch.alloc(max_grid * n_slots * kMlpThreads);
-  if (c->H == 64) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
+  if (tc_eligible(c)) c->tc_scratch.alloc((int64_t)c->num_sms * 2 * std::max<int64_t>(c->K, 1) * (16 * 128 * 4 + 128));
   if (c->ps_ready.size() != (size_t)M) c->ps_ready.assign((size_t)M, 0);
   c->fact_blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (c->rows + kFactRows - 1) / kFactRows),
                                           (int64_t)c->num_sms * 2);  // 112 KB shared memory: two per SM
@@ -706,7 +706,8 @@ void zero_empty_rows(hgnn_ctx* c, float* a) {
   check_launch(c);
 }
 
-bool use_tc_bwd(const hgnn_ctx* c) { return c->bwd_impl == 1 && c->H == 64; }
+// H = 32 runs zero-padded on the 64-wide backward kernel (HL = 32)
+bool use_tc_bwd(const hgnn_ctx* c) { return c->bwd_impl == 1 && tc_eligible(c); }
 bool use_fact_bwd(const hgnn_ctx* c) { return use_tc_bwd(c) && use_fact(c); }
 
 int tc_bwd_grid(const hgnn_ctx* c, int64_t n_rows) {
@@ -725,6 +726,13 @@ int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
   args.prof = c->prof_on ? c->prof.p + (edge ? 0 : kProfCount) : nullptr;
   const int grid = tc_bwd_grid(c, args.n_rows);
   const bool prof = args.prof != nullptr;
+  if (c->H == 32) {  // zero-padded H = 32 instance
+    auto k32 = edge ? mlp_tc_backward_kernel<kEdgeInput, false, 32> : mlp_tc_backward_kernel<kNodeInput, false, 32>;
+    CUDA_OK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
+    k32<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(args);
+    check_launch(c);
+    return grid;
+  }
   if (c->bwd_split && !prof) {  // split-row epilogue (mlp_tc_bwd_cs.cuh)
     auto ks = mode == kEdgeFact ? mlp_tc_backward_cs_kernel<kEdgeFact>
                                 : (edge ? mlp_tc_backward_cs_kernel<kEdgeInput> : mlp_tc_backward_cs_kernel<kNodeInput>);
@@ -1493,15 +1501,16 @@ int hgnn_params_upload(hgnn_ctx* c, const double* flat, int64_t count) {
     if (tc_eligible(c)) {
       std::vector<float> ch, bch;
       int64_t nf = 0, nb = 0;
-      const bool with_bwd = H == 64;
+      const bool with_bwd = true;  // H = 32: zero-padded 64-wide backward chunks
       mp_chunk_plan(H, K, c->M, with_bwd, [](bool, int64_t, int64_t, bool) {}, c->chunk_off, c->bchunk_off, nf, nb);
       ch.resize((size_t)nf);
       bch.resize((size_t)nb);
       mp_chunk_plan(
           H, K, c->M, with_bwd,
           [&](bool fwd, int64_t pos, int64_t src, bool lo) {
-            const float hi = tf32_rna_host(p[(size_t)src]);
-            (fwd ? ch : bch)[(size_t)pos] = lo ? tf32_rna_host(p[(size_t)src] - hi) : hi;
+            const float w = src < 0 ? 0.f : p[(size_t)src];  // src -1: zero padding
+            const float hi = tf32_rna_host(w);
+            (fwd ? ch : bch)[(size_t)pos] = lo ? tf32_rna_host(w - hi) : hi;
           },
           c->chunk_off, c->bchunk_off, nf, nb);
       c->chunks.upload(ch.data(), nf, c->stream);

@@ -283,6 +283,28 @@ void chunk_layout_bwd(int in_dim, int H, int K, int64_t base, Emit&& emit, int s
   for (int c = seg0; c < seg0 + nseg; ++c)
     chunk([&](int n, int kk) { return c * H + n < in_dim ? W(0) + (int64_t)(c * H + n) * H + kk : (int64_t)-1; });
 }
+// The backward sequence of an H = 32 MLP run zero-padded on the 64-wide
+// kernel (mlp_tc_bwd.cuh, HL = 32): same order as chunk_layout_bwd, 64 x 64
+// chunks whose entries outside the HL x HL blocks are padding (src -1).
+template <class Emit>
+void chunk_layout_bwd_pad(int in_dim, int HL, int K, int64_t base, Emit&& emit) {
+  constexpr int P = 64;
+  const int nseg = in_dim / HL;
+  auto chunk = [&](auto src_of) {
+    for (int kk = 0; kk < P; ++kk)
+      for (int n = 0; n < P; ++n) {
+        const int64_t src = (n < HL && kk < HL) ? src_of(n, kk) : (int64_t)-1;
+        emit(base + tc_chunk_index(n, kk, P), src, false);
+        emit(base + tc_chunk_index(P + n, kk, P), src, true);
+      }
+    base += 2 * (int64_t)P * P;
+  };
+  auto W = [&](int l) { return mlp_w_offset(l, in_dim, HL); };
+  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * HL + kk) * HL + n; });
+  for (int l = 1; l <= K; ++l) chunk([&](int n, int kk) { return W(l) + (int64_t)kk * HL + n; });
+  for (int l = K + 1; l >= 1; --l) chunk([&](int n, int kk) { return W(l) + (int64_t)n * HL + kk; });
+  for (int c = 0; c < nseg; ++c) chunk([&](int n, int kk) { return W(0) + (int64_t)(c * HL + n) * HL + kk; });
+}
 inline int64_t chunk_floats_fwd(int in_dim, int H, int K, int nseg = -1) {
   return (int64_t)((nseg < 0 ? in_dim / H : nseg) + K + 1) * 2 * H * H;
 }
@@ -293,9 +315,9 @@ inline int64_t chunk_floats_bwd(int in_dim, int H, int K, int nseg = -1) {
 // Every tcgen05 weight-chunk sequence of the MP block, in buffer order: per
 // layer m the edge MLP (3 input segments), the node MLP, and the factorised
 // edge MLP (kEdgeFact: e segment only); fwd offsets at [3 m + {0, 1, 2}], the
-// backward sequences (H = 64) likewise. emit(fwd?, pos, src, lo) places
+// backward sequences (H = 64, or H = 32 zero-padded to 64) likewise. emit(fwd?, pos, src, lo) places
 // element src of the MP parameter block; the same code serves the host upload
-// and the device refresh maps of the Adam step.
+// and the device refresh maps of the Adam step (src -1: zero padding).
 template <class Emit>
 void mp_chunk_plan(int H, int K, int64_t M, bool with_bwd, Emit&& emit, std::vector<int64_t>& fwd_off,
                    std::vector<int64_t>& bwd_off, int64_t& fwd_total, int64_t& bwd_total) {
@@ -315,9 +337,14 @@ void mp_chunk_plan(int H, int K, int64_t M, bool with_bwd, Emit&& emit, std::vec
       fwd_total += chunk_floats_fwd(in_dim, H, K, nseg);
       if (with_bwd) {
         bwd_off.push_back(bwd_total);
-        chunk_layout_bwd(in_dim, H, K, bwd_total,
-                         [&](int64_t pos, int64_t src, bool lo) { emit(false, pos, poff + src, lo); }, seg0, nseg);
-        bwd_total += chunk_floats_bwd(in_dim, H, K, nseg);
+        auto e = [&](int64_t pos, int64_t src, bool lo) { emit(false, pos, src < 0 ? src : poff + src, lo); };
+        if (H == 64) {
+          chunk_layout_bwd(in_dim, H, K, bwd_total, e, seg0, nseg);
+          bwd_total += chunk_floats_bwd(in_dim, H, K, nseg);
+        } else {  // H = 32: zero-padded 64-wide sequence (no factorised variant: an empty slot)
+          if (v != 2) chunk_layout_bwd_pad(in_dim, H, K, bwd_total, e);
+          if (v != 2) bwd_total += chunk_floats_bwd(in_dim / H * 64, 64, K);
+        }
       }
     }
     off = off_node + mlp_param_count(2 * H, H, K);

@@ -135,9 +135,33 @@ enum { kProfTotal = 0, kProfW = 1, kProfA = 2, kProfSt = 3, kProfDwE = 4, kProfF
        kProfEpiTotal = 8, kProfEpiRecompute = 9, kProfEpiFlush = 10, kProfEpiStage = 11, kProfEpiDb = 12,
        kProfEpiWaitDx = 13, kProfEpiLnBwd = 14, kProfEpiInput = 15, kProfCount = 16 };
 
-template <int MODE>
+// HL-wide row (HL = 32: the zero-padded H = 32 instance) into v[0, 64)
+template <int HL>
+__device__ __forceinline__ void bwd_row(const float* p, float (&v)[64]) {
+#pragma unroll
+  for (int q = 0; q < HL / 8; ++q) ptx::ldg256(p + 8 * q, v + 8 * q);
+#pragma unroll
+  for (int j = HL; j < 64; ++j) v[j] = 0.f;
+}
+
+template <int MODE, int HL = 64>
 __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64]) {
   if (HGNN_EXP & 16) valid = false;
+  if (HL != 64) {  // kEdgeInput / kNodeInput rows of width HL, zero-padded
+    if (!valid) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = 0.f;
+      return;
+    }
+    const float* seg;
+    if (MODE == kEdgeInput)
+      seg = c == 0 ? a.x + (int64_t)__ldg(a.src + row) * HL
+                   : (c == 1 ? a.x + (int64_t)__ldg(a.dst + row) * HL : a.e_in + row * HL);
+    else
+      seg = c == 0 ? a.a + row * HL : a.x + row * HL;
+    bwd_row<HL>(seg, v);
+    return;
+  }
   TcFwdArgs f{};
   f.src = a.src;
   f.dst = a.dst;
@@ -294,21 +318,47 @@ __device__ __forceinline__ float2 warp_colsum64(const float (&v)[64]) {
   return make_float2(a[0], a[1]);
 }
 
+// Parameter-free LayerNorm over the first HL of 64 values (kernels.cpp:81-94);
+// the padding columns [HL, 64) become 0. Returns inv_std.
+template <int HL>
+__device__ __forceinline__ float ln0_pad(float (&v)[64]) {
+  if (HL == 64) return ln0_tree<64>(v);
+  float m[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < HL; ++j) m[j % 4] += v[j];
+  const float mean = ((m[0] + m[1]) + (m[2] + m[3])) * (1.0f / HL);
+  float q[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < HL; ++j) {
+    const float d = v[j] - mean;
+    q[j % 4] = fmaf(d, d, q[j % 4]);
+  }
+  const float inv_std = ptx::rsqrt_fast(((q[0] + q[1]) + (q[2] + q[3])) * (1.0f / HL) + 1e-12f);
+#pragma unroll
+  for (int j = 0; j < 64; ++j) v[j] = j < HL ? (v[j] - mean) * inv_std : 0.f;
+  return inv_std;
+}
+
 __device__ __forceinline__ int colsum_base(int lane) {
   return 32 * ((lane >> 4) & 1) + 16 * ((lane >> 3) & 1) + 8 * ((lane >> 2) & 1) + 4 * ((lane >> 1) & 1) +
          2 * (lane & 1);
 }
 
-template <int MODE, bool PROF>
+// HL: logical hidden width. 64, or 32 for the H = 32 processor MLPs
+// (kEdgeInput / kNodeInput) run zero-padded to 64: padded weight chunks,
+// rows of width HL in HBM, LayerNorms over the first HL columns, padding
+// columns forced to 0, gradients written in the HL-wide parameter layout.
+template <int MODE, bool PROF, int HL = 64>
 __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(TcBwdArgs a) {
   using Cfg = TcBwdCfg;
   constexpr int H = Cfg::H;
+  static_assert(HL == 64 || (HL == 32 && (MODE == kEdgeInput || MODE == kNodeInput)), "padded width: 3-segment MLPs");
   constexpr bool FACT = MODE == kEdgeFact;
   constexpr bool ENC = MODE == kEncoder;
   constexpr bool DEC = MODE == kDecoder;
   constexpr bool EDGE = MODE != kNodeInput && !ENC && !DEC;
   constexpr int nseg = MODE == kEdgeInput ? 3 : (MODE == kNodeInput ? 2 : 1);
-  const int in_dim = ENC ? a.in_dim : (DEC ? H : (MODE == kNodeInput ? 2 : 3) * H);  // parameter layout
+  const int in_dim = ENC ? a.in_dim : (DEC ? H : (MODE == kNodeInput ? 2 : 3) * HL);  // parameter layout
   constexpr int seg0 = FACT ? 2 : 0;                         // W0 row block of the first input segment
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -336,7 +386,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   const int n_dw = K + 1 + nseg;            // dW jobs per pair
   const int64_t n_tiles = (a.n_rows + 127) / 128;
   const int64_t n_pairs = (n_tiles + 1) / 2;
-  const int64_t n_par = (ENC || DEC) ? a.n_par : mlp_param_count(in_dim, H, K);
+  const int64_t n_par = (ENC || DEC) ? a.n_par : mlp_param_count(in_dim, HL, K);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::WSTAGES; ++s) {
@@ -361,7 +411,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
   }
   // biases of the recomputed linears 0..K (the output bias has no backward use)
   for (int i = threadIdx.x; i < (K + 1) * H; i += blockDim.x)
-    sbias[i] = __ldg(a.params + mlp_b_offset(i / H, in_dim, H) + (i % H));
+    sbias[i] = i % H < HL ? __ldg(a.params + mlp_b_offset(i / H, in_dim, HL) + (i % H)) : 0.f;
   if (warp == 8) ptx::tmem_alloc<512>(tmem_base_slot);
   ptx::tc_fence_before();
   __syncthreads();
@@ -404,17 +454,18 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const long long tf0 = PROF ? clock64() : 0;
       const int jj = (int)(jf % n_dw);
       const int lin = jj <= K ? K + 1 - jj : 0;
-      const int rowbase = jj <= K ? 0 : (jj - K - 1 + seg0) * H;
+      const int rowbase = jj <= K ? 0 : (jj - K - 1 + seg0) * HL;
       const bool with_db = jj <= K + 1;
       const int acc = kDwN128 ? 0 : (int)(jf & 1);
       ptx::mbar_wait(&dw_full[acc], kDwN128 ? (uint32_t)(jf & 1) : (uint32_t)((jf >> 1) & 1));
       ptx::tc_fence_after();
       const int c0 = 32 * g;
-      float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow) * H + c0
-                         : gpart1 + mlp_w_offset(lin, in_dim, H) + (int64_t)(rowbase + trow - 64) * H + c0;
+      float* gw = wq < 2 ? gpart0 + mlp_w_offset(lin, in_dim, HL) + (int64_t)(rowbase + trow) * HL + c0
+                         : gpart1 + mlp_w_offset(lin, in_dim, HL) + (int64_t)(rowbase + trow - 64) * HL + c0;
       // kEncoder: rows >= in_dim of dW0 belong to the zero padding; kDecoder:
       // dW_{k+1} is H x out_dim (columns >= out_dim are padding)
-      const bool w_ok = (!ENC || lin > 0 || (wq < 2 ? trow : trow - 64) < in_dim) && !(DEC && lin == K + 1);
+      const bool w_ok = (!ENC || lin > 0 || (wq < 2 ? trow : trow - 64) < in_dim) && !(DEC && lin == K + 1) &&
+                        (HL == 64 || ((wq < 2 ? trow : trow - 64) < HL && c0 < HL));
       float p0[16], p1[16];
       if (kDwN128) {  // columns c and 64 + c: (row block) x d_hi and x d_lo
         float q0[16], q1[16];
@@ -462,8 +513,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         }
         if (warp == 0 && trow < a.out_dim)
           asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + wk + H * a.out_dim + trow), "f"(dbs) : "memory");
-      } else if (with_db && warp < 2) {
-        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, H) + trow), "f"(dbs)
+      } else if (with_db && warp < 2 && trow < HL) {
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(gpart0 + mlp_b_offset(lin, in_dim, HL) + trow), "f"(dbs)
                      : "memory");
       }
       if (PROF) pf[2] += (unsigned long long)(clock64() - tf0);
@@ -509,18 +560,18 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const long long tr0 = PROF ? clock64() : 0;
       // ---------------------------------------------- forward recompute
       // (segment c + 1 is gathered while the MMA of segment c runs)
-      if (!HGNN_BWD_PREFETCH || !h_ready) bwd_gather<MODE>(a, row, valid, 0, h);
+      if (!HGNN_BWD_PREFETCH || !h_ready) bwd_gather<MODE, HL>(a, row, valid, 0, h);
 #pragma unroll 1
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
           ptx::mbar_wait(&a_empty[g], pe);
           pe ^= 1;
           ptx::tc_fence_after();
-          if (!HGNN_BWD_PREFETCH) bwd_gather<MODE>(a, row, valid, c, h);
+          if (!HGNN_BWD_PREFETCH) bwd_gather<MODE, HL>(a, row, valid, c, h);
         }
         bwd_store_a(t_ahi, t_alo, h);
         tc_signal(&a_full[g]);
-        if (HGNN_BWD_PREFETCH && c + 1 < nseg) bwd_gather<MODE>(a, row, valid, c + 1, h);
+        if (HGNN_BWD_PREFETCH && c + 1 < nseg) bwd_gather<MODE, HL>(a, row, valid, c + 1, h);
       }
       if (FACT) bwd_gather_proj(a, row, valid, h);  // P_s[src] + P_d[dst], during the e W0_e MMA
       ptx::mbar_wait(&d_full[g], pd);
@@ -542,7 +593,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         ptx::tc_fence_after();
         float u[H];
         bwd_load_d(t_d, sbias + l * H, u);
-        const float inv_std = (kExp & 8) ? 1.0f : ln0_tree<H>(u);
+        const float inv_std = (kExp & 8) ? 1.0f : ln0_pad<HL>(u);
         float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
 #pragma unroll
         for (int q = 0; q < 16; ++q)
@@ -556,10 +607,10 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       if (valid) {
         if (EDGE) {  // d_y = de + inv_d * d_a[dst] (model.cpp:354-360)
           const float s = __ldg(a.inv_deg + row);
-          const float* da = a.d_a + (int64_t)__ldg(a.dst + row) * H;
-          const float4* de = a.de_in ? reinterpret_cast<const float4*>(a.de_in + row * H) : nullptr;
+          const float* da = a.d_a + (int64_t)__ldg(a.dst + row) * HL;
+          const float4* de = a.de_in ? reinterpret_cast<const float4*>(a.de_in + row * HL) : nullptr;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {  // de: read, later rewritten in place: coherent path
+          for (int q = 0; q < HL / 8; ++q) {  // de: read, later rewritten in place: coherent path
             float x1[8];
             ptx::ldg256(da + 8 * q, x1);
 #pragma unroll
@@ -571,6 +622,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
               dh[8 * q + 4 * u + 3] = fmaf(s, x1[4 * u + 3], x2.w);
             }
           }
+#pragma unroll
+          for (int j = HL; j < H; ++j) dh[j] = 0.f;
         } else if (DEC) {
 #pragma unroll
           for (int j = 0; j < H; ++j) dh[j] = 0.f;
@@ -578,8 +631,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           for (int j = 0; j < 8; ++j)
             if (j < a.out_dim) dh[j] = __ldg(a.d_out + row * a.out_dim + j);
         } else {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) ptx::ldg256(a.d_out + row * H + 8 * q, dh + 8 * q);
+          bwd_row<HL>(a.d_out + row * HL, dh);
         }
       } else {
 #pragma unroll
@@ -600,6 +652,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           const float inv_std = (kExp & 2) ? 1.0f : scr_inv[(l - 1) * 128 + trow];
           const long long tl0 = PROF ? clock64() : 0;
           bwd_store_raw(t_d, dh);  // residual d_h pre-loaded into the accumulator
+          static_assert(!HGNN_PK_LNB || HL == 64, "packed LN adjoint: H = 64 only");
           if constexpr (HGNN_PK_LNB) {
           // ELU adjoint (kernels.cpp:68-71), residual rebuild h_{l-1} = h_l - ELU(t_l),
           // LN adjoint (kernels.cpp:99-126), on packed pairs
@@ -631,8 +684,8 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           }
           const float2 s1 = f2_add(f2_add(p1[0], p1[1]), f2_add(p1[2], p1[3]));
           const float2 s2 = f2_add(f2_add(p2[0], p2[1]), f2_add(p2[2], p2[3]));
-          const float g_mean = (s1.x + s1.y) * (1.0f / H);
-          const float gx_mean = (s2.x + s2.y) * (1.0f / H);
+          const float g_mean = (s1.x + s1.y) * (1.0f / HL);
+          const float gx_mean = (s2.x + s2.y) * (1.0f / HL);
           const float2 ngx = make_float2(-gx_mean, -gx_mean), ngm = make_float2(-g_mean, -g_mean);
           const float2 is2 = make_float2(inv_std, inv_std);
 #pragma unroll
@@ -665,12 +718,16 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
             }
           }
           const float g_mean =
-              (((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]))) * (1.0f / H);
+              (((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]))) * (1.0f / HL);
           const float gx_mean =
-              (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / H);
+              (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / HL);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
+            if (4 * q >= HL) {  // zero padding
+              dh[4 * q] = dh[4 * q + 1] = dh[4 * q + 2] = dh[4 * q + 3] = 0.f;
+              continue;
+            }
             dh[4 * q] = (dh[4 * q] - g_mean - t4.x * gx_mean) * inv_std;  // kernels.cpp:99-126
             dh[4 * q + 1] = (dh[4 * q + 1] - g_mean - t4.y * gx_mean) * inv_std;
             dh[4 * q + 2] = (dh[4 * q + 2] - g_mean - t4.z * gx_mean) * inv_std;
@@ -699,15 +756,15 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
 #pragma unroll
           for (int q = 0; q < 8; ++q) ptx::stg256_hint(a.dy_out + row * H + 8 * q, dh + 8 * q, once);
         }
-        if (c >= 0 && !HGNN_BWD_PREFETCH) bwd_gather<MODE>(a, row, valid, c, h);  // dW0 segment operand
+        if (c >= 0 && !HGNN_BWD_PREFETCH) bwd_gather<MODE, HL>(a, row, valid, c, h);  // dW0 segment operand
         stage_chunk(h, dh);
         if (HGNN_BWD_PREFETCH && jb >= K) {  // h is dead: fetch the next dW0 segment operand, or the next
           if (c + 1 < nseg) {                // tile's first input segment, behind the dX wait
-            bwd_gather<MODE>(a, row, valid, c + 1, h);
+            bwd_gather<MODE, HL>(a, row, valid, c + 1, h);
           } else {
             const int64_t nrow = (2 * (pair + gridDim.x) + g) * 128 + trow;
             h_ready = pair + gridDim.x < n_pairs;
-            if (h_ready) bwd_gather<MODE>(a, nrow, nrow < a.n_rows, 0, h);
+            if (h_ready) bwd_gather<MODE, HL>(a, nrow, nrow < a.n_rows, 0, h);
           }
         }
         wait_dx();
@@ -721,13 +778,13 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           else if (DEC) outp = a.d_x_out;
           else outp = c == 0 ? a.d_a_out : a.d_x_out;
 #pragma unroll
-          for (int cc = 0; cc < (ENC ? 0 : H); cc += 16) {  // kEncoder: the feature adjoint is not needed
+          for (int cc = 0; cc < (ENC ? 0 : HL); cc += 16) {  // kEncoder: the feature adjoint is not needed
             float p[16];
             ptx::tmem_ld16(t_d + cc, p);
             ptx::tmem_wait_ld();
             if (valid) {
-              ptx::stg256_hint(outp + row * H + cc, p, once);
-              ptx::stg256_hint(outp + row * H + cc + 8, p + 8, once);
+              ptx::stg256_hint(outp + row * HL + cc, p, once);
+              ptx::stg256_hint(outp + row * HL + cc + 8, p + 8, once);
             }
           }
           if (c + 1 < nseg) tc_signal(&a_full[g]);  // D consumed; A (= split d_h) stays

@@ -416,13 +416,13 @@ void build_refresh_maps(hgnn_ctx* c) {
   if (tc_eligible(c)) {
     std::vector<int64_t> fo, bo;
     int64_t nf = 0, nb = 0;
-    mp_chunk_plan(H, K, c->M, H == 64, [](bool, int64_t, int64_t, bool) {}, fo, bo, nf, nb);
+    mp_chunk_plan(H, K, c->M, true, [](bool, int64_t, int64_t, bool) {}, fo, bo, nf, nb);
     ch.resize((size_t)nf);
     bch.resize((size_t)nb);
     mp_chunk_plan(
-        H, K, c->M, H == 64,
+        H, K, c->M, true,
         [&](bool fwd, int64_t pos, int64_t src, bool lo) {
-          (fwd ? ch : bch)[(size_t)pos] = (uint32_t)src | (lo ? 0x80000000u : 0u);
+          (fwd ? ch : bch)[(size_t)pos] = src < 0 ? 0x7fffffffu : ((uint32_t)src | (lo ? 0x80000000u : 0u));
         },
         fo, bo, nf, nb);
   }

@@ -194,10 +194,11 @@ def test_tensor_core_forward_matches_simt_and_oracle(engine, H, k):
         assert rel(outs[impl][1], ref["e_out"][0][M - 1]) < FWD_TOL, impl
 
 
-@pytest.mark.parametrize("E,p,k,M", [(3, 3, 5, 2), (3, 5, 2, 1), (2, 4, 0, 1), (4, 5, 5, 2)])
-def test_tensor_core_backward_matches_simt_and_oracle(engine, E, p, k, M):
-    """tcgen05 3xTF32 MLP backward (dX chain + stacked dW MMAs) vs SIMT vs fp64 oracle."""
-    H = 64
+@pytest.mark.parametrize("E,p,k,M,H", [(3, 3, 5, 2, 64), (3, 5, 2, 1, 64), (2, 4, 0, 1, 64), (4, 5, 5, 2, 64),
+                                       (3, 3, 5, 2, 32), (4, 3, 3, 2, 32), (3, 4, 0, 1, 32), (5, 3, 5, 4, 32)])
+def test_tensor_core_backward_matches_simt_and_oracle(engine, E, p, k, M, H):
+    """tcgen05 3xTF32 MLP backward (dX chain + stacked dW MMAs) vs SIMT vs fp64
+    oracle; H = 32 runs zero-padded on the 64-wide kernel (mlp_tc_bwd.cuh HL)."""
     cfg = GnnConfig("tcb", H, M, k, mode="na2a")
     g = build_rank_graph(E, p, 1, 0, "verify")
     mp = mp_params(cfg, init_params(cfg, 21))
