@@ -230,6 +230,8 @@ def main():
     ap.add_argument("--halo-sm-reserve", type=int, default=-1, help="SMs left to the exchange (-1: engine default)")
     ap.add_argument("--fact", type=int, default=-1, choices=[-1, 0, 1],
                     help="edge_factorized option (-1: engine default)")
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="extra engine option (hgnn_set_option), e.g. tma_gather=0 (A/B runs)")
     ap.add_argument("--halo-overlap", type=int, default=1, choices=[0, 1],
                     help="1: forward exchange on a side stream, overlapped with the interior edges (N > 1)")
     a = ap.parse_args()
@@ -276,6 +278,9 @@ def main():
         eng.set_option("halo_sm_reserve", a.halo_sm_reserve)
     if a.fact >= 0:
         eng.set_option("edge_factorized", a.fact)
+    for kv in a.opt:
+        k_, v_ = kv.split("=", 1)
+        eng.set_option(k_, int(v_))
     eng.synthetic_inputs(seed=1234)
     stream = torch.cuda.ExternalStream(eng.stream_ptr)
 

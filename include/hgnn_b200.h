@@ -87,6 +87,11 @@ typedef struct hgnn_host_graph hgnn_host_graph;
 /* factors: (Rx,Ry,Rz) for HGNN_PART_BLOCK, or NULL for balanced_factors. */
 int hgnn_graph_build(int64_t elements_per_axis, int64_t poly_order, int64_t num_ranks, int strategy,
                      const int64_t* factors, int32_t rank, hgnn_host_graph** out);
+/* Same on the box [domain_min, domain_max] (MeshConfig::domain_min / domain_max,
+ * mesh.hpp; NULL = the unit cube). HGNN_ERR_CONFIG unless max > min per axis. */
+int hgnn_graph_build_domain(int64_t elements_per_axis, int64_t poly_order, int64_t num_ranks, int strategy,
+                            const int64_t* factors, int32_t rank, const double* domain_min,
+                            const double* domain_max, hgnn_host_graph** out);
 void hgnn_graph_free(hgnn_host_graph* g);
 /* Zero-copy view of the built arrays (valid until hgnn_graph_free). */
 int hgnn_graph_view(const hgnn_host_graph* g, hgnn_graph_desc* out);
@@ -220,8 +225,11 @@ int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double
  *                     3-segment edge kernels + aggregate + dx gather.
  * "mlp_forward_impl": 1 = tcgen05 tensor-core MLP forward (default, H in {32,64}),
  *                     0 = SIMT fp32 kernels.
- * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H = 64),
- *                      0 = SIMT fp32 kernels.
+ * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H in {32, 64};
+ *                      H = 32 runs zero-padded on the 64-wide kernel), 0 = SIMT fp32.
+ * "tma_gather":        1 = the fused edge forward's input rows gathered by TMA
+ *                      tile::gather4 into SMEM (H = 64); 0 = (default, measured
+ *                      faster) per-thread 256-bit row loads into registers.
  * "encoder_impl":      1 = (default, H = 64 with both MLP impls 1) node / edge
  *                      encoders on the tcgen05 MLP kernels (zero-padded F-feature
  *                      input, skip + output LayerNorm in the epilogue); 0 = SIMT.

@@ -175,6 +175,8 @@ def ref_lib() -> C.CDLL:
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_graph_build.restype = vp
         lib.ref_graph_build.argtypes = [C.c_int64] * 3 + [C.c_int] + [C.c_int64] * 3 + [C.c_int]
+        lib.ref_graph_build_domain.restype = vp
+        lib.ref_graph_build_domain.argtypes = [C.c_int64] * 3 + [C.c_int] + [C.c_int64] * 3 + [C.c_int, f64p, f64p]
         lib.ref_graph_free.argtypes = [vp]
         lib.ref_graph_save_binary.argtypes = [vp, C.c_int, C.c_char_p]
         lib.ref_has_io.restype = C.c_int
@@ -214,10 +216,15 @@ class RefRankGraph:
 class RefGraph:
     STRAT = {"slab": 0, "block": 1, "verify": 2}
 
-    def __init__(self, E, p, R, strategy="verify", factors=None, features=True):
+    def __init__(self, E, p, R, strategy="verify", factors=None, features=True, domain=None):
         lib = ref_lib()
         f = factors or (0, 0, 0)
-        self.h = lib.ref_graph_build(E, p, R, self.STRAT[strategy], f[0], f[1], f[2], int(features))
+        if domain is None:
+            self.h = lib.ref_graph_build(E, p, R, self.STRAT[strategy], f[0], f[1], f[2], int(features))
+        else:  # MeshConfig::domain_min / domain_max
+            lo, hi = (C.c_double * 3)(*domain[0]), (C.c_double * 3)(*domain[1])
+            self.h = lib.ref_graph_build_domain(E, p, R, self.STRAT[strategy], f[0], f[1], f[2], int(features),
+                                                C.cast(lo, f64p), C.cast(hi, f64p))
         if not self.h:
             raise RuntimeError(lib.ref_last_error().decode())
         self.R = R

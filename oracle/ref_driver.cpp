@@ -193,13 +193,18 @@ const char* ref_last_error() { return g_err.c_str(); }
 
 // strategy: 0 slab, 1 block (factors fx,fy,fz if fx>0 else balanced_factors),
 // 2 = verify_partition (harness.cpp:42-45: slab at R=1, balanced block otherwise)
-void* ref_graph_build(int64_t E, int64_t p, int64_t R, int strategy, int64_t fx, int64_t fy, int64_t fz,
-                      int attach_features) {
+void* ref_graph_build_domain(int64_t E, int64_t p, int64_t R, int strategy, int64_t fx, int64_t fy, int64_t fz,
+                             int attach_features, const double* dmin, const double* dmax) {
   RefGraph* rg = nullptr;
   const int rc = guarded([&] {
     auto owned = std::make_unique<RefGraph>();
     owned->mc.elements_per_axis = E;
     owned->mc.poly_order = p;
+    if (dmin && dmax)
+      for (int a = 0; a < 3; ++a) {
+        owned->mc.domain_min[a] = dmin[a];
+        owned->mc.domain_max[a] = dmax[a];
+      }
     const Mesh mesh = build_box_mesh(owned->mc);
     PartitionMap part;
     if (strategy == 0) part = partition_mesh(mesh, R, PartitionStrategy::Slab);
@@ -211,6 +216,11 @@ void* ref_graph_build(int64_t E, int64_t p, int64_t R, int strategy, int64_t fx,
     rg = owned.release();
   });
   return rc == 0 ? rg : nullptr;
+}
+
+void* ref_graph_build(int64_t E, int64_t p, int64_t R, int strategy, int64_t fx, int64_t fy, int64_t fz,
+                      int attach_features) {
+  return ref_graph_build_domain(E, p, R, strategy, fx, fy, fz, attach_features, nullptr, nullptr);
 }
 
 void ref_graph_free(void* h) { delete static_cast<RefGraph*>(h); }

@@ -117,6 +117,8 @@ def _load() -> C.CDLL:
     sig = {
         "hgnn_last_error": (C.c_char_p, []),
         "hgnn_graph_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, i64p, C.c_int32, C.POINTER(vp)]),
+        "hgnn_graph_build_domain": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, i64p, C.c_int32, f64p, f64p,
+                                              C.POINTER(vp)]),
         "hgnn_graph_free": (None, [vp]),
         "hgnn_graph_view": (C.c_int, [vp, C.POINTER(GraphDesc)]),
         "hgnn_graph_save_binary": (C.c_int, [C.POINTER(GraphDesc), C.c_char_p]),
@@ -166,7 +168,7 @@ def _load() -> C.CDLL:
 
 
 LIB = _load()
-EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_free", "hgnn_graph_view", "hgnn_graph_save_binary",
+EXPORTED = ["hgnn_last_error", "hgnn_graph_build", "hgnn_graph_build_domain", "hgnn_graph_free", "hgnn_graph_view", "hgnn_graph_save_binary",
             "hgnn_graph_load_binary", "hgnn_balanced_factors",
             "hgnn_param_count", "hgnn_init_params", "hgnn_mp_param_range", "hgnn_device_count", "hgnn_nccl_unique_id",
             "hgnn_ctx_create", "hgnn_local_group_create", "hgnn_local_group_destroy", "hgnn_local_group_set_timeout",

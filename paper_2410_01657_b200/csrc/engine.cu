@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include "edge_fact.cuh"
 #include "engine_ctx.hpp"
 #include "graph_kernels.cuh"
@@ -660,8 +662,44 @@ void edge_proj(hgnn_ctx* c, int64_t m, const float* x) {
   c->ps_ready[(size_t)m] = 1;
 }
 
-// The fused edge update (kEdgeFact): tiles [t0, t1) of the segment table;
-// writes e' (es[m + 1]) and the aggregate of every receiver in those tiles.
+// 2-D fp32 tensor map over a rows x H row-major buffer for TMA tile::gather4
+// (box 32 floats x 1 row, 128-byte swizzle). The driver entry point comes
+// from the runtime (no libcuda link dependency).
+CUtensorMap row_tensor_map(const float* base, int64_t rows, int H) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) fail(HGNN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)H * sizeof(float)};
+  const cuuint32_t box[2] = {32, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(HGNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+template <int MODE>
+void launch_fused_tma(hgnn_ctx* c, const TcFwdArgs& args) {
+  using Cfg = TcCfg<64>;
+  auto k = mlp_tc_forward_tma_kernel<64, MODE>;
+  CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_TMA));
+  const CUtensorMap tx = row_tensor_map(args.x, c->rows, 64), te = row_tensor_map(args.e_in, c->ne, 64);
+  const int64_t pairs = (args.n_tiles + 1) / 2;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pairs, c->num_sms - c->sm_reserve));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM_TMA, c->stream>>>(args, tx, te);
+  check_launch(c);
+}
+
+// The fused edge update (kEdgeFact / kEdgeFused): tiles [t0, t1) of the
+// segment table; writes e' and the aggregate of every receiver in those tiles.
 template <int H, int MODE>
 void launch_fused_typed(hgnn_ctx* c, const TcFwdArgs& args) {
   auto k = mlp_tc_forward_kernel<H, MODE, false>;
@@ -692,7 +730,10 @@ void launch_fused_forward(hgnn_ctx* c, int64_t m, int64_t t0, int64_t t1, const 
   args.chunks = c->chunks.p + c->chunk_off[(size_t)(3 * m + (fact ? 2 : 0))];
   args.params = layer_params(c, m, true).p;
   args.k = (int)c->K;
-  if (c->H == 64) {
+  if (c->H == 64 && c->tma_gather) {
+    if (fact) launch_fused_tma<kEdgeFact>(c, args);
+    else launch_fused_tma<kEdgeFused>(c, args);
+  } else if (c->H == 64) {
     if (fact) launch_fused_typed<64, kEdgeFact>(c, args);
     else launch_fused_typed<64, kEdgeFused>(c, args);
   } else {
@@ -1695,6 +1736,9 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value <= 0) fail(HGNN_ERR_CONFIG, "collective_timeout_ms must be positive");
       c->coll_timeout_ms = value;
       if (c->group) c->group->timeout_ms = value;
+    } else if (k == "tma_gather") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "tma_gather: 0 (per-thread row loads) or 1 (TMA gather4)");
+      c->tma_gather = (int)value;
     } else if (k == "encoder_impl") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "encoder_impl: 0 (simt) or 1 (tcgen05, H = 64)");
       c->enc_impl = (int)value;

@@ -129,6 +129,7 @@ struct hgnn_ctx {
   // the fused edge kernel ([0, n_tiles_bnd) cover the boundary slots), rows
   // with an empty segment (zeroed aggregate), node projections per layer
   int edge_fact = 0;              // option "edge_factorized"
+  int tma_gather = 0;             // option "tma_gather": fused edge forward input rows by TMA tile::gather4 (H = 64; measured slower, off)
   bool fact_ok = false;           // every receiver segment fits one 128-slot tile
   hgnn_b200::DevBuf<int32_t> tiles, rows_empty;
   int64_t n_tiles = 0, n_tiles_bnd = 0, n_rows_empty = 0;

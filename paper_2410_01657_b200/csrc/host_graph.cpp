@@ -185,10 +185,13 @@ void build_csr(HostGraph& hg, int64_t rows) {
   csr(hg.edge_src, hg.out_off, hg.out_edges);
 }
 
+// dmin / dmax: MeshConfig::domain_min / domain_max (mesh.hpp, default the unit cube)
 std::unique_ptr<HostGraph> build(int64_t E, int64_t p, int64_t R, int strategy, const int64_t* factors,
-                                 int32_t rank) {
+                                 int32_t rank, const double* dmin, const double* dmax) {
   if (E < 1) fail(HGNN_ERR_CONFIG, "MeshConfig: elements_per_axis must be >= 1");
   if (p < 1) fail(HGNN_ERR_CONFIG, "MeshConfig: poly_order must be >= 1");
+  for (int a = 0; a < 3; ++a)  // MeshConfig::validate (mesh.cpp:12-14)
+    if (!(dmax[a] > dmin[a])) fail(HGNN_ERR_CONFIG, "MeshConfig: domain_max must exceed domain_min on every axis");
   if (R < 1) fail(HGNN_ERR_PARTITION, "partition: rank count must be >= 1");
   if (rank < 0 || rank >= R) fail(HGNN_ERR_PARTITION, "assemble_rank_graph: rank out of range");
   const int64_t n1d = E * p + 1;
@@ -352,7 +355,6 @@ std::unique_ptr<HostGraph> build(int64_t E, int64_t p, int64_t R, int strategy, 
   // ---- positions (lattice_position, mesh.cpp:86-104) incl. mirrored halo rows.
   {
     const std::vector<double> gll = gll_points(p);
-    const double h = (1.0 - 0.0) / static_cast<double>(E);
     hg->positions.resize(static_cast<size_t>(rows * 3));
     for (int64_t i = 0; i < nl; ++i) {
       int64_t g[3];
@@ -363,8 +365,9 @@ std::unique_ptr<HostGraph> build(int64_t E, int64_t p, int64_t R, int strategy, 
           elem = E - 1;
           loc = p;
         }
+        const double h = (dmax[a] - dmin[a]) / static_cast<double>(E);
         hg->positions[static_cast<size_t>(i * 3 + a)] =
-            0.0 + static_cast<double>(elem) * h + 0.5 * (gll[static_cast<size_t>(loc)] + 1.0) * h;
+            dmin[a] + static_cast<double>(elem) * h + 0.5 * (gll[static_cast<size_t>(loc)] + 1.0) * h;
       }
     }
     for (int64_t hr = 0; hr < nh; ++hr) {
@@ -636,14 +639,21 @@ extern "C" {
 
 const char* hgnn_last_error(void) { return g_last_error.c_str(); }
 
-int hgnn_graph_build(int64_t E, int64_t p, int64_t R, int strategy, const int64_t* factors, int32_t rank,
-                     hgnn_host_graph** out) {
+int hgnn_graph_build_domain(int64_t E, int64_t p, int64_t R, int strategy, const int64_t* factors, int32_t rank,
+                            const double* domain_min, const double* domain_max, hgnn_host_graph** out) {
   return guarded([&] {
     if (!out) fail(HGNN_ERR_CONFIG, "hgnn_graph_build: null output handle");
+    static const double unit_min[3] = {0.0, 0.0, 0.0}, unit_max[3] = {1.0, 1.0, 1.0};
     auto h = std::make_unique<hgnn_host_graph>();
-    h->g = build(E, p, R, strategy, factors, rank);
+    h->g = build(E, p, R, strategy, factors, rank, domain_min ? domain_min : unit_min,
+                 domain_max ? domain_max : unit_max);
     *out = h.release();
   });
+}
+
+int hgnn_graph_build(int64_t E, int64_t p, int64_t R, int strategy, const int64_t* factors, int32_t rank,
+                     hgnn_host_graph** out) {
+  return hgnn_graph_build_domain(E, p, R, strategy, factors, rank, nullptr, nullptr, out);
 }
 
 void hgnn_graph_free(hgnn_host_graph* g) { delete g; }

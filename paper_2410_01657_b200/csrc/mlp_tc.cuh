@@ -30,6 +30,8 @@
 // e' is never re-read and no atomics are used.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "mlp_simt.cuh"
 #include "tc_ptx.cuh"
 
@@ -53,6 +55,14 @@ struct TcCfg {
   static constexpr size_t SMEM = OFF_Y + 1024;                         // + biases (k <= 16)
   static constexpr size_t SMEM_FACT = OFF_Y + 2 * 128 * H * 4 + 1024;
   static constexpr size_t SMEM_ENC = OFF_Y + 10 * H * 4 + 1024;       // kEncoder: skip W (<= 8 x H), LN gamma, beta
+  // fused edge kernel with TMA-gathered input rows (mlp_tc_forward_tma_kernel):
+  // 2 weight stages, output tiles, one 128-row gather buffer per slot
+  static constexpr int T_STAGES = 2;
+  static constexpr size_t T_OFF_BARS = (size_t)T_STAGES * CHUNK_BYTES;
+  static constexpr size_t T_OFF_BIAS = T_OFF_BARS + 256;
+  static constexpr size_t T_OFF_Y = (T_OFF_BIAS + 18 * H * 4 + 1023) / 1024 * 1024;
+  static constexpr size_t T_OFF_GX = T_OFF_Y + 2 * 128 * H * 4;
+  static constexpr size_t SMEM_TMA = T_OFF_GX + 2 * 128 * H * 4 + 1024;
 };
 
 // Index (in floats) of B element (n, k) inside a chunk (K-major core matrices).
@@ -275,8 +285,31 @@ __device__ __forceinline__ uint32_t ytile_off(int r, int c) {
   return (uint32_t)(r * H * 4 + ((c ^ (r & 7)) << 4));
 }
 
-template <int H, int MODE, bool PROF>
-__global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(TcFwdArgs a) {
+#ifndef HGNN_PRODUCER_SLEEP_NS
+#define HGNN_PRODUCER_SLEEP_NS 100
+#endif
+// TMA tile::gather4: rows i0..i3 of a 2-D tensor map (box 32 floats x 1 row,
+// 128-byte swizzle), columns [col, col + 32), into 4 consecutive 128-byte
+// smem rows, completing on bar.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int col, int i0, int i1, int i2, int i3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(i0), "r"(i1), "r"(i2), "r"(i3), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+// TMAG (fused edge modes, H = 64): the input segments of each tile are
+// gathered by TMA (tile::gather4 over the receiver-sorted slots' src / dst
+// indices, or the slots' own e rows) into a per-slot 128-row SMEM buffer
+// (two 16 KB halves, 128-byte swizzle), issued by warp 9 between its weight
+// chunk loads, and the epilogue reads its row from SMEM right before the
+// operand store — coalesced 128-byte TMA requests instead of per-thread row
+// loads through L1, and segment 0 of the next tile lands during the current
+// tile's hidden layers.
+template <int H, int MODE, bool PROF, bool TMAG>
+__device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CUtensorMap* tmx, const CUtensorMap* tme) {
   using Cfg = TcCfg<H>;
   constexpr bool FACT = MODE == kEdgeFact;
   constexpr bool FUSED = MODE == kEdgeFact || MODE == kEdgeFused;  // segment tiles + in-kernel aggregate
@@ -285,21 +318,29 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   constexpr int nseg = (MODE == kEdgeFact || ENC || DEC) ? 1 : (MODE == kNodeInput ? 2 : 3);
   // parameter layout (kEdgeFact: the 3H-input MLP; kEncoder: F input features)
   const int in_dim = ENC ? a.in_dim : (DEC ? H : (MODE == kNodeInput ? 2 : 3) * H);
+  static_assert(!TMAG || (FUSED && H == 64), "TMA gathers: fused edge modes at H = 64");
+  constexpr int STAGES = TMAG ? Cfg::T_STAGES : Cfg::STAGES;
+  constexpr size_t OFF_BARS = TMAG ? Cfg::T_OFF_BARS : Cfg::OFF_BARS;
+  constexpr size_t OFF_BIAS = TMAG ? Cfg::T_OFF_BIAS : Cfg::OFF_BIAS;
+  constexpr size_t OFF_Y = TMAG ? Cfg::T_OFF_Y : Cfg::OFF_Y;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* wring = reinterpret_cast<float*>(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BARS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BARS);
   uint64_t* w_full = bars;                    // [STAGES]
-  uint64_t* w_empty = bars + Cfg::STAGES;     // [STAGES]
-  uint64_t* a_full = bars + 2 * Cfg::STAGES;  // [2]
+  uint64_t* w_empty = bars + STAGES;          // [STAGES]
+  uint64_t* a_full = bars + 2 * STAGES;       // [2]
   uint64_t* a_empty = a_full + 2;             // [2]
   uint64_t* d_full = a_empty + 2;             // [2]
   uint64_t* y_full = d_full + 2;              // [2] kEdgeFact: output tile written (4 epilogue warps)
   uint64_t* y_empty = y_full + 2;             // [2] kEdgeFact: output tile consumed (reducer warp)
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(y_empty + 2);
-  float* sbias = reinterpret_cast<float*>(smem + Cfg::OFF_BIAS);  // (k+2) x H
-  uint8_t* ytile = smem + Cfg::OFF_Y;                             // kEdgeFact: [2][128][H] swizzled
-  float* senc = reinterpret_cast<float*>(smem + Cfg::OFF_Y);       // kEncoder: W_skip [8][H], gamma, beta
+  uint64_t* gx_full = y_empty + 2;            // [2] TMAG: gather buffer landed (TMA transaction bytes)
+  uint64_t* gx_empty = gx_full + 2;           // [2] TMAG: gather buffer read (4 epilogue warps)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(gx_empty + 2);
+  float* sbias = reinterpret_cast<float*>(smem + OFF_BIAS);  // (k+2) x H
+  uint8_t* ytile = smem + OFF_Y;                             // kEdgeFact: [2][128][H] swizzled
+  float* senc = reinterpret_cast<float*>(smem + OFF_Y);       // kEncoder: W_skip [8][H], gamma, beta
+  uint8_t* gx = smem + Cfg::T_OFF_GX;                         // TMAG: [2][2 halves][128][32] swizzled
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -318,7 +359,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < Cfg::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&w_full[s], 1);
       ptx::mbar_init(&w_empty[s], 1);
     }
@@ -328,6 +369,8 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       ptx::mbar_init(&d_full[s], 1);
       ptx::mbar_init(&y_full[s], 4);
       ptx::mbar_init(&y_empty[s], 1);
+      ptx::mbar_init(&gx_full[s], 1);
+      ptx::mbar_init(&gx_empty[s], 4);
     }
     ptx::fence_mbarrier_init();
   }
@@ -366,6 +409,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
 
   if (warp < 8) {
     // ------------------------------------------------------------ epilogue
+    uint32_t pgx = 0;  // TMAG: gx_full phase of this slot
     const int g = warp / 4;   // tile slot
     const int wq = warp % 4;  // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
@@ -390,8 +434,27 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     float v[H];
     const int trow = 32 * wq + lane;  // row inside the tile
     uint32_t py = 0;                  // y_empty phase (kEdgeFact)
+    // TMAG: this thread's row of the slot's gather buffer (128-byte swizzle:
+    // 16-byte chunk j of row r at r * 128 + ((j ^ r % 8) << 4)); conflict-free
+    auto read_seg = [&](bool valid_row) {
+      ptx::mbar_wait(&gx_full[g], pgx);
+      pgx ^= 1;
+      const uint8_t* rb = gx + (size_t)g * (128 * H * 4) + trow * 128;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 t = *reinterpret_cast<const float4*>(rb + hf * (128 * 128) + ((j ^ (trow & 7)) << 4));
+          v[32 * hf + 4 * j] = valid_row ? t.x : 0.f;
+          v[32 * hf + 4 * j + 1] = valid_row ? t.y : 0.f;
+          v[32 * hf + 4 * j + 2] = valid_row ? t.z : 0.f;
+          v[32 * hf + 4 * j + 3] = valid_row ? t.w : 0.f;
+        }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&gx_empty[g]);
+    };
     int64_t pair = blockIdx.x;
-    if (pair < n_pairs) {
+    if (!TMAG && pair < n_pairs) {
       int64_t b0, e0;
       tile_rows(2 * pair + g, b0, e0);
       tc_gather<H, MODE>(a, b0 + trow, b0 + trow < e0, 0, v);
@@ -413,9 +476,10 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
           ptx::tc_fence_after();
           if (PROF) e_ae += (unsigned long long)(clock64() - t0);
         }
+        if (TMAG) read_seg(valid);
         tc_store_a<H>(t_ahi, t_alo, v);
         signal_a();
-        if (c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v);
+        if (!TMAG && c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v);
       }
       if (FACT) tc_gather_proj<H>(a, row, valid, v);  // node-end projections, during the e W0_e MMA
       wait_d();
@@ -454,7 +518,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
       tc_store_a<H>(t_ahi, t_alo, h);
       signal_a();
       const int64_t next = pair + gridDim.x;
-      if (next < n_pairs) {
+      if (!TMAG && next < n_pairs) {
         int64_t nb, ne_;
         tile_rows(2 * next + g, nb, ne_);
         tc_gather<H, MODE>(a, nb + trow, nb + trow < ne_, 0, v);
@@ -594,7 +658,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
             if (PROF) i_m += (unsigned long long)(clock64() - t0);
           }
           ptx::mma_commit_w(&w_empty[ws]);
-          if (++ws == Cfg::STAGES) {
+          if (++ws == STAGES) {
             ws = 0;
             wph ^= 1;
           }
@@ -661,7 +725,86 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     }
   } else {
     // ------------------------------------------------------------ weight loader (warp 9; 10-11 idle)
-    if (warp == 9 && lane == 0) {
+    if (TMAG && warp == 9) {
+      // Weight chunks (lane 0) and the input-row gathers (all lanes), polled
+      // in turn: a gather of segment c for slot g is issued once the slot's
+      // buffer is read (per slot in its epilogue's consumption order: per
+      // pair, per segment); lane L gathers rows 4L .. 4L + 3 of the
+      // tile (indices clamped to its last row) as two tile::gather4 (columns
+      // 0-31 / 32-63), and expect_tx covers the groups issued.
+      int ws = 0, wj = 0, gc[2] = {0, 0};
+      uint32_t wph = 0, pge[2] = {0, 0};
+      int64_t wp = blockIdx.x, gp[2] = {blockIdx.x, blockIdx.x};
+      // prepared next gather per slot: row groups, this lane's 4 row indices, e rows?
+      int ngr[2] = {0, 0}, nix[2][4];
+      bool nes[2] = {false, false};
+      auto prep = [&](int gg) {
+        if (gp[gg] >= n_pairs) return;
+        int64_t tb, te;
+        tile_rows(2 * gp[gg] + gg, tb, te);
+        const int n = (int)(te - tb);
+        ngr[gg] = (n + 3) / 4;
+        nes[gg] = FACT || gc[gg] == 2;  // the slots' own e rows
+        const int32_t* ix = gc[gg] == 0 ? a.src : a.dst;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = 4 * lane + i < n ? 4 * lane + i : n - 1;
+          nix[gg][i] = (nes[gg] || lane >= ngr[gg]) ? (int)(tb + r) : __ldg(ix + tb + r);
+        }
+      };
+      prep(0);
+      prep(1);
+      const long long t0 = clock64();
+      while (wp < n_pairs || gp[0] < n_pairs || gp[1] < n_pairs) {
+        bool idle = true;  // nothing issued this round: back off (the warp shares its issue slots with an epilogue warp)
+        if (wp < n_pairs) {
+          const bool ok = __shfl_sync(0xffffffffu, lane == 0 ? (int)ptx::mbar_test_wait(&w_empty[ws], wph ^ 1) : 0, 0);
+          if (ok) {
+            idle = false;
+            if (lane == 0) {
+              ptx::mbar_arrive_expect_tx(&w_full[ws], Cfg::CHUNK_BYTES);
+              ptx::bulk_g2s(wring + (size_t)ws * Cfg::CHUNK_FLOATS, a.chunks + (size_t)wj * Cfg::CHUNK_FLOATS,
+                            Cfg::CHUNK_BYTES, &w_full[ws]);
+            }
+            if (++ws == STAGES) {
+              ws = 0;
+              wph ^= 1;
+            }
+            if (++wj == n_chunks) {
+              wj = 0;
+              wp += gridDim.x;
+            }
+          }
+        }
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {  // per slot: its own cursor (pair gp[gg], segment gc[gg])
+          if (gp[gg] >= n_pairs) continue;
+          const bool ok =
+              __shfl_sync(0xffffffffu, lane == 0 ? (int)ptx::mbar_test_wait(&gx_empty[gg], pge[gg] ^ 1) : 0, 0);
+          if (!ok) continue;
+          idle = false;
+          pge[gg] ^= 1;
+          if (lane == 0) ptx::mbar_arrive_expect_tx(&gx_full[gg], (uint32_t)ngr[gg] * 2 * 512);
+          __syncwarp();
+          if (lane < ngr[gg]) {
+            uint8_t* dst = gx + (size_t)gg * (128 * H * 4) + lane * 512;
+            const CUtensorMap* map = nes[gg] ? tme : tmx;
+            tma_gather4(dst, map, 0, nix[gg][0], nix[gg][1], nix[gg][2], nix[gg][3], &gx_full[gg]);
+            tma_gather4(dst + 128 * 128, map, 32, nix[gg][0], nix[gg][1], nix[gg][2], nix[gg][3], &gx_full[gg]);
+          }
+          if (++gc[gg] == nseg) {
+            gc[gg] = 0;
+            gp[gg] += gridDim.x;
+          }
+          prep(gg);  // the slot's next gather: its indices load while the buffer is in use
+        }
+        if (idle) __nanosleep(HGNN_PRODUCER_SLEEP_NS);
+        if (clock64() - t0 > 40000000000ll) {  // watchdog, as mbar_wait
+          if (lane == 0) printf("hgnn_b200: gather producer timeout (block %d)\n", (int)blockIdx.x);
+          __trap();
+        }
+      }
+    } else if (!TMAG && warp == 9 && lane == 0) {
       int ws = 0;
       uint32_t wph = 0;
       for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
@@ -670,7 +813,7 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
           ptx::mbar_arrive_expect_tx(&w_full[ws], Cfg::CHUNK_BYTES);
           ptx::bulk_g2s(wring + (size_t)ws * Cfg::CHUNK_FLOATS, a.chunks + (size_t)j * Cfg::CHUNK_FLOATS,
                         Cfg::CHUNK_BYTES, &w_full[ws]);
-          if (++ws == Cfg::STAGES) {
+          if (++ws == STAGES) {
             ws = 0;
             wph ^= 1;
           }
@@ -684,6 +827,19 @@ __global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(Tc
     ptx::tc_fence_after();
     ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
   }
+}
+
+template <int H, int MODE, bool PROF>
+__global__ void __launch_bounds__(TcCfg<H>::THREADS, 1) mlp_tc_forward_kernel(TcFwdArgs a) {
+  mlp_tc_forward_body<H, MODE, PROF, false>(a, nullptr, nullptr);
+}
+// fused edge modes with TMA-gathered input rows; tmx over x (rows x H),
+// tme over e (N_e x H): 2-D fp32, box 32 x 1, 128-byte swizzle
+template <int H, int MODE>
+__global__ void __launch_bounds__(TcCfg<H>::THREADS, 1)
+    mlp_tc_forward_tma_kernel(TcFwdArgs a, const __grid_constant__ CUtensorMap tmx,
+                              const __grid_constant__ CUtensorMap tme) {
+  mlp_tc_forward_body<H, MODE, false, true>(a, &tmx, &tme);
 }
 
 }  // namespace hgnn_b200

@@ -42,7 +42,10 @@ struct TcBwdCfg {
   static constexpr uint32_t SBO = 128;
   static constexpr uint32_t LO_OFF = (H / 8) * 128;
   static constexpr int WSTAGES = 2;
-  static constexpr int NSTAGE = 4;                     // dW staging buffers
+#ifndef HGNN_BWD_NSTAGE
+#define HGNN_BWD_NSTAGE 4
+#endif
+  static constexpr int NSTAGE = HGNN_BWD_NSTAGE;       // dW staging buffers
   static constexpr int STAGE_BYTES = 32 * 1024;        // A (16 KB) + B (16 KB), 32 rows
   // MN-major SWIZZLE_128B_BASE32B staging: atoms of 4 K-rows x 128 B of MN,
   // 32-byte granule g of atom row r stored at granule g ^ r.

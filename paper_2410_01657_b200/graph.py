@@ -81,14 +81,19 @@ def _arr(ptr, n, dtype):
 
 
 def build_rank_graph(elements_per_axis: int, poly_order: int, num_ranks: int, rank: int,
-                     strategy: str = "verify", factors=None) -> RankGraph:
-    """One rank's reduced graph and halo map for the unit-cube GLL box mesh."""
+                     strategy: str = "verify", factors=None, domain_min=None, domain_max=None) -> RankGraph:
+    """One rank's reduced graph and halo map for the GLL box mesh on
+    [domain_min, domain_max] (MeshConfig, default the unit cube)."""
     h = C.c_void_p()
     fac = None
     if factors is not None:
         fac = (C.c_int64 * 3)(*factors)
-    N.check(N.LIB.hgnn_graph_build(elements_per_axis, poly_order, num_ranks, STRATEGIES[strategy],
-                                   C.cast(fac, N.i64p) if fac is not None else None, rank, C.byref(h)))
+    lo = (C.c_double * 3)(*domain_min) if domain_min is not None else None
+    hi = (C.c_double * 3)(*domain_max) if domain_max is not None else None
+    N.check(N.LIB.hgnn_graph_build_domain(elements_per_axis, poly_order, num_ranks, STRATEGIES[strategy],
+                                          C.cast(fac, N.i64p) if fac is not None else None, rank,
+                                          C.cast(lo, N.f64p) if lo is not None else None,
+                                          C.cast(hi, N.f64p) if hi is not None else None, C.byref(h)))
     return _take(h)
 
 

@@ -286,3 +286,31 @@ def test_memory_lean_plan_matches_standard(engine):
     assert rel(res[1][0], ref["x_out"][0][M - 1]) < FWD_TOL
     assert rel(res[1][3], ref["de_in"][0][0]) < BWD_TOL
     assert grad_rel(res[1][4], ref["grads"][0], cfg) < BWD_TOL
+
+
+@pytest.mark.parametrize("E,p,M,k,fact", [(3, 5, 2, 5, 0), (4, 3, 2, 2, 1), (2, 4, 1, 0, 0)])
+def test_tma_gathered_forward_is_bitwise_equal(engine, E, p, M, k, fact):
+    """Fused edge forward with TMA tile::gather4 input rows (option tma_gather 1)
+    against per-thread 256-bit row loads (0, default): the same arithmetic on the
+    same operands, so outputs, aggregates and the backward are bitwise equal."""
+    H = 64
+    cfg = GnnConfig("tma", H, M, k, mode="na2a")
+    g = build_rank_graph(E, p, 1, 0, "verify")
+    mp = mp_params(cfg, init_params(cfg, 41))
+    x0, e0, dx, de = random_inputs(g, H, 23)
+    res = {}
+    for tma in (1, 0):
+        engine.upload_graph(g)
+        engine.configure(cfg)
+        engine.upload_params(mp)
+        engine.set_option("edge_factorized", fact)
+        engine.set_option("tma_gather", tma)
+        x_out, e_out = engine.nmp_forward(x0, e0, want_e=True)
+        a0 = engine.trace(0, "a_sync")
+        res[tma] = (x_out, e_out, a0) + tuple(engine.nmp_backward(dx, de))
+    engine.set_option("tma_gather", 0)
+    engine.set_option("edge_factorized", 0)
+    for u, v in zip(res[1], res[0]):
+        assert np.asarray(u).tobytes() == np.asarray(v).tobytes()
+    ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
+    assert rel(res[1][0], ref["x_out"][0][M - 1]) < FWD_TOL

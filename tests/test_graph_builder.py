@@ -53,6 +53,26 @@ def test_graphs_match_reference_build(E, p, R, strat, fac):
         assert g.max_buffer_rows == ref.ranks[r].max_buffer_rows
 
 
+@pytest.mark.skipif(not O.ref_available(), reason="reference not built in place (oracle/_ref)")
+@pytest.mark.parametrize("E,p,R,strat,dom", [(4, 2, 2, "slab", ((-1.0, 0.0, 2.0), (1.0, 0.5, 5.0))),
+                                             (4, 3, 4, "verify", ((0.25, -3.0, 0.0), (2.0, 3.0, 0.1)))])
+def test_graphs_match_reference_build_on_a_domain(E, p, R, strat, dom):
+    """MeshConfig::domain_min / domain_max (mesh.cpp:86-104): positions and every
+    other array bit-exact on a non-unit box."""
+    ref = O.RefGraph(E, p, R, strat, None, features=False, domain=dom)
+    for r in range(R):
+        g = build_rank_graph(E, p, R, r, strat, None, dom[0], dom[1])
+        for f in FIELDS:
+            assert getattr(g, f).tobytes() == getattr(ref.ranks[r], f).tobytes(), (r, f)
+
+
+def test_domain_must_be_a_box():
+    """MeshConfig::validate (mesh.cpp:12-14): ConfigError unless max > min on every axis."""
+    from paper_2410_01657_b200 import ConfigError
+    with pytest.raises(ConfigError):
+        build_rank_graph(2, 2, 1, 0, "slab", None, (0.0, 0.0, 0.0), (1.0, 0.0, 1.0))
+
+
 def test_params_match_reference_hashes(golden):
     for key, want in golden["params"].items():
         H, M, k, s = [int(t[1:]) for t in key.split("_")]
