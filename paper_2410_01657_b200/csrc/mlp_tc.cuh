@@ -207,7 +207,7 @@ __device__ __forceinline__ void tc_signal(uint64_t* bar) {
 }
 
 #ifndef HGNN_EXP
-#define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py); bit 32: forward input gathers dropped
+#define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py); bits 32: input gathers dropped, 64: no e' stores, 128: no reducer work
 #endif
 
 template <int H, int MODE>
@@ -683,7 +683,7 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
     for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
       int64_t tb, te;
       tile_rows(2 * pair + g, tb, te);
-      const int n = (int)(te - tb);
+      const int n = (HGNN_EXP & 128) ? 0 : (int)(te - tb);
       ptx::mbar_wait(&y_full[g], pf);
       pf ^= 1;
       float acc[CPL];
@@ -700,7 +700,7 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
           const int32_t d = __shfl_sync(0xffffffffu, d_l, i);
           const int32_t dn = __shfl_sync(0xffffffffu, dn_l, i);
           const float w = __shfl_sync(0xffffffffu, w_l, i);
-          float* eo = a.out ? a.out + (tb + r) * H + CPL * lane : nullptr;  // nullptr: e' not stored (dead)
+          float* eo = (a.out && !(HGNN_EXP & 64)) ? a.out + (tb + r) * H + CPL * lane : nullptr;  // nullptr: e' not stored (dead)
           if (CPL == 2) {
             const float2 y = *reinterpret_cast<const float2*>(yt + ytile_off<H>(r, lane / 2) + 8 * (lane & 1));
             if (eo) *reinterpret_cast<float2*>(eo) = y;
