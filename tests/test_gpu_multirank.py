@@ -96,7 +96,7 @@ def test_two_gpu_parity_and_consistency(gpus, R, E, p, H, M, k, mode):
         # gradients only regrouped (two launches' partials)
         assert res[r]["dx0"].tobytes() == res[r]["dx0_serial"].tobytes()
         assert res[r]["de0"].tobytes() == res[r]["de0_serial"].tobytes()
-        assert rel(res[r]["grads"], res[r]["grads_serial"]) < 1e-5
+        assert rel(res[r]["grads"], res[r]["grads_serial"]) < 1e-4  # fp32 partials regrouped
     if mode == "none":
         return
     # consistency: coincident copies bitwise equal, R-rank == 1-rank by gid
