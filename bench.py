@@ -84,6 +84,13 @@ def node_flops(H, k):
     return 2 * H * H * (3 + k)
 
 
+def edge_flops_fact(H, k):
+    """Per edge in the factorised edge kernels (edge_factorized = 1): the input
+    linear's x_src / x_dst blocks run at node level (edge_proj, node-level
+    adjoint), the edge kernels multiply e W0_e, the k hidden and the output linear."""
+    return 2 * H * H * (2 + k)
+
+
 # --------------------------------------------------------------------------
 # clocks (nvidia-smi sampled during the timed region)
 # --------------------------------------------------------------------------
@@ -364,7 +371,9 @@ def main():
     # ---- roofline of the dominant kernel class (live CUDA-event durations)
     per_launch = {c: (t / max(nl_, 1), nl_) for c, (t, nl_) in ktimes.items()}
     step_share = {c: t / a.steps / ms for c, (t, _) in ktimes.items()}
-    flops = {"edge_bwd": g.num_edges * 2 * edge_flops(H, k), "edge_fwd": g.num_edges * edge_flops(H, k),
+    fact_used = ktimes.get("edge_proj", (0.0, 0))[1] > 0  # factorised edge kernels ran
+    ef = edge_flops_fact(H, k) if fact_used else edge_flops(H, k)
+    flops = {"edge_bwd": g.num_edges * 2 * ef, "edge_fwd": g.num_edges * ef,
              "node_bwd": g.num_local * 2 * node_flops(H, k), "node_fwd": g.num_local * node_flops(H, k)}
     dom = max(flops, key=lambda c: ktimes[c][0])
     peaks = json.load(open(ROOT / "MEASURED_PEAKS.json")) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -384,7 +393,10 @@ def main():
                 "peak_basis": "dense TF32 = 1/2 of measured sustained bf16 (MEASURED_PEAKS.json)",
                 "flops_per_launch": flops[dom], "ms_per_launch": avg_ms,
                 "pipe": ("tcgen05 kind::tf32 3xTF32 (3 tensor products per algorithmic product; the backward "
-                         "kernel also recomputes the forward: algorithmic flops exclude both)")}
+                         "kernel also recomputes the forward: algorithmic flops exclude both)"),
+                "edge_flops_basis": ("factorised: 2H^2(2+k) per edge and direction (the x_src / x_dst blocks of "
+                                     "the input linear run at node level)") if fact_used else
+                ("3-segment: 2H^2(4+k) per edge and direction")}
 
     # ---- HBM-bound kernels: algorithmic bytes per step / live kernel time per step
     hbm_peak = peaks.get("hbm_gbs") or 7700.0

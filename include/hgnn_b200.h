@@ -216,7 +216,7 @@ int hgnn_compute_gradients(hgnn_ctx* ctx, double* loss, double* grads, double* y
 int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double eps, double* loss);
 
 /* ---- options --------------------------------------------------------------- */
-/* "edge_factorized":  1 = (tcgen05 paths; default 0) the edge MLP's input linear is
+/* "edge_factorized":  1 = (default; tcgen05 paths, H = 64) the edge MLP's input linear is
  *                     split through the nodes, P = x [W0_s | W0_d] once per node and
  *                     only e W0_e per edge; the forward edge kernel also forms the
  *                     aggregate (one fused kernel, no aggregate launch) and the

@@ -133,11 +133,22 @@ __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
       const int64_t i = base + r;
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
       if (i < rows) {
+        // slot order, four slots' loads in flight at a time (the twin index and
+        // the dY row of one slot are a dependent pair; the sum order is unchanged)
+        // (slots past the segment end add +0: s starts at +0 and never becomes -0,
+        // so the padding leaves every sum bitwise unchanged)
         const int32_t p1 = __ldg(end + i);
-        for (int32_t p = __ldg(beg + i); p < p1; ++p) {
-          const int64_t e = src_half ? (int64_t)__ldg(twin + p) : (int64_t)p;
-          const float4 v = __ldg(reinterpret_cast<const float4*>(dy + e * H) + cc);
-          s = make_float4(s.x + v.x, s.y + v.y, s.z + v.z, s.w + v.w);
+        for (int32_t p = __ldg(beg + i); p < p1; p += 4) {
+          int64_t e[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            e[u] = p + u < p1 ? (src_half ? (int64_t)__ldg(twin + p + u) : (int64_t)(p + u)) : (int64_t)-1;
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            v[u] = e[u] >= 0 ? __ldg(reinterpret_cast<const float4*>(dy + e[u] * H) + cc) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s = make_float4(s.x + v[u].x, s.y + v[u].y, s.z + v[u].z, s.w + v[u].w);
         }
       }
       *reinterpret_cast<float4*>(sr + r * NS + 4 * c4) = s;

@@ -128,7 +128,7 @@ struct hgnn_ctx {
   // factorised edge MLP (kEdgeFact, edge_fact.cuh): receiver-segment tiles of
   // the fused edge kernel ([0, n_tiles_bnd) cover the boundary slots), rows
   // with an empty segment (zeroed aggregate), node projections per layer
-  int edge_fact = 0;              // option "edge_factorized"
+  int edge_fact = 1;              // option "edge_factorized" (default on: measured faster at C3)
   int tma_gather = 0;             // option "tma_gather": fused edge forward input rows by TMA tile::gather4 (H = 64; measured slower, off)
   bool fact_ok = false;           // every receiver segment fits one 128-slot tile
   hgnn_b200::DevBuf<int32_t> tiles, rows_empty;

@@ -279,7 +279,7 @@ def test_memory_lean_plan_matches_standard(engine):
             with pytest.raises(UninitializedError):  # the backward consumed the trace storage
                 engine.trace(0, "e_in")
     engine.set_option("memory_lean", -1)
-    engine.set_option("edge_factorized", 0)
+    engine.set_option("edge_factorized", 1)  # the default
     for u, v in zip(res[0], res[1]):
         assert u.tobytes() == v.tobytes()
     ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx])
@@ -309,7 +309,7 @@ def test_tma_gathered_forward_is_bitwise_equal(engine, E, p, M, k, fact):
         a0 = engine.trace(0, "a_sync")
         res[tma] = (x_out, e_out, a0) + tuple(engine.nmp_backward(dx, de))
     engine.set_option("tma_gather", 0)
-    engine.set_option("edge_factorized", 0)
+    engine.set_option("edge_factorized", 1)  # the default
     for u, v in zip(res[1], res[0]):
         assert np.asarray(u).tobytes() == np.asarray(v).tobytes()
     ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
