@@ -125,33 +125,42 @@ __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
   for (int64_t base = (int64_t)blockIdx.x * kFactRows; base < rows; base += (int64_t)gridDim.x * kFactRows) {
     __syncthreads();
     // segment sums, item (r, c4): lanes 0-15 of a warp read the twin row
-    // (S_src), lanes 16-31 the slot row (S_dst): 256-byte coalesced pieces
-    for (int t = threadIdx.x; t < kFactRows * NS / 4; t += blockDim.x) {
-      const int r = t / (NS / 4), c4 = t % (NS / 4);
+    // (S_src), lanes 16-31 the slot row (S_dst): 256-byte coalesced pieces.
+    // A thread owns column piece c4 of rows r0, r0 + 8, ..., r0 + 56 and walks
+    // their 8 segments together, slot offset u at a time: 8 independent
+    // twin-index -> dY-row load pairs in flight (each row still summed in slot
+    // order; slots past a segment's end add +0, which leaves the sum bitwise
+    // unchanged since it starts at +0 and never becomes -0).
+    {
+      static_assert(kFactThreads == 256 && kFactRows == 64 && NS / 4 == 32, "item layout: 8 rows per thread");
+      const int c4 = threadIdx.x % (NS / 4), r0 = threadIdx.x / (NS / 4);
       const bool src_half = c4 < H / 4;
       const int cc = src_half ? c4 : c4 - H / 4;
-      const int64_t i = base + r;
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < rows) {
-        // slot order, four slots' loads in flight at a time (the twin index and
-        // the dY row of one slot are a dependent pair; the sum order is unchanged)
-        // (slots past the segment end add +0: s starts at +0 and never becomes -0,
-        // so the padding leaves every sum bitwise unchanged)
-        const int32_t p1 = __ldg(end + i);
-        for (int32_t p = __ldg(beg + i); p < p1; p += 4) {
-          int64_t e[4];
+      int32_t pb[8], pe[8];
+      float4 s[8];
+      int maxd = 0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            e[u] = p + u < p1 ? (src_half ? (int64_t)__ldg(twin + p + u) : (int64_t)(p + u)) : (int64_t)-1;
-          float4 v[4];
+      for (int j = 0; j < 8; ++j) {
+        const int64_t i = base + r0 + 8 * j;
+        pb[j] = i < rows ? __ldg(beg + i) : 0;
+        pe[j] = i < rows ? __ldg(end + i) : 0;
+        s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        maxd = max(maxd, pe[j] - pb[j]);
+      }
+      for (int u = 0; u < maxd; ++u) {
+        int64_t e[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            v[u] = e[u] >= 0 ? __ldg(reinterpret_cast<const float4*>(dy + e[u] * H) + cc) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < 8; ++j)
+          e[j] = pb[j] + u < pe[j] ? (src_half ? (int64_t)__ldg(twin + pb[j] + u) : (int64_t)(pb[j] + u)) : (int64_t)-1;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) s = make_float4(s.x + v[u].x, s.y + v[u].y, s.z + v[u].z, s.w + v[u].w);
+        for (int j = 0; j < 8; ++j) {
+          const float4 v =
+              e[j] >= 0 ? __ldg(reinterpret_cast<const float4*>(dy + e[j] * H) + cc) : make_float4(0.f, 0.f, 0.f, 0.f);
+          s[j] = make_float4(s[j].x + v.x, s[j].y + v.y, s[j].z + v.z, s[j].w + v.w);
         }
       }
-      *reinterpret_cast<float4*>(sr + r * NS + 4 * c4) = s;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) *reinterpret_cast<float4*>(sr + (r0 + 8 * j) * NS + 4 * c4) = s[j];
     }
     for (int t = threadIdx.x; t < kFactRows * H / 4; t += blockDim.x) {
       const int r = t / (H / 4), c = t % (H / 4);
