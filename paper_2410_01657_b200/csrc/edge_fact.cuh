@@ -147,11 +147,17 @@ __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
         s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         maxd = max(maxd, pe[j] - pb[j]);
       }
+      // the twin indices of slot offset u + 1 load while the dY rows of u do
+      int32_t tw[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) tw[j] = (src_half && pb[j] < pe[j]) ? __ldg(twin + pb[j]) : 0;
       for (int u = 0; u < maxd; ++u) {
         int64_t e[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          e[j] = pb[j] + u < pe[j] ? (src_half ? (int64_t)__ldg(twin + pb[j] + u) : (int64_t)(pb[j] + u)) : (int64_t)-1;
+        for (int j = 0; j < 8; ++j) {
+          e[j] = pb[j] + u < pe[j] ? (src_half ? (int64_t)tw[j] : (int64_t)(pb[j] + u)) : (int64_t)-1;
+          tw[j] = (src_half && pb[j] + u + 1 < pe[j]) ? __ldg(twin + pb[j] + u + 1) : 0;
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float4 v =
