@@ -1,7 +1,7 @@
-# timing ablation: fused-forward reducer (64: no e' stores, 128: no reducer work)
+# timing ablation on the factorised default: backward gather prefetch
 set -x
-for v in "" 64 128; do
+for v in "" pf; do
   tag=${v:-default}
   if [ -n "$v" ]; then export HGNN_B200_LIB=paper_2410_01657_b200/lib/exp/libhgnn_b200_exp$v.so; else unset HGNN_B200_LIB; fi
-  timeout 600 python bench.py --steps 3 --warmup 3 --profile > gpurun_out/ab_$tag.json 2>&1; echo rc=$?
+  for i in 1 2; do timeout 600 python bench.py --steps 3 --warmup 3 --profile > gpurun_out/ab_${tag}_$i.json 2>&1; echo rc=$?; done
 done
