@@ -41,7 +41,10 @@ struct TcBwdCfg {
   static constexpr uint32_t LBO = (2 * H / 8) * 128;   // K-major weight chunks
   static constexpr uint32_t SBO = 128;
   static constexpr uint32_t LO_OFF = (H / 8) * 128;
-  static constexpr int WSTAGES = 2;
+#ifndef HGNN_BWD_WSTAGES
+#define HGNN_BWD_WSTAGES 2
+#endif
+  static constexpr int WSTAGES = HGNN_BWD_WSTAGES;
 #ifndef HGNN_BWD_NSTAGE
 #define HGNN_BWD_NSTAGE 4
 #endif
