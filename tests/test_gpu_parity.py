@@ -171,6 +171,17 @@ def test_backward_before_forward_is_uninitialized(gpus):
     eng.close()
 
 
+def test_option_values_are_validated(engine):
+    """hgnn_set_option: unknown keys and out-of-range values raise ConfigError
+    (the engine's state is unchanged)."""
+    from paper_2410_01657_b200 import ConfigError
+    for key, bad in [("edge_factorized", 2), ("memory_lean", 3), ("encoder_impl", -1), ("tma_gather", 5),
+                     ("mlp_backward_split", 2), ("mlp_backward_impl", 7), ("halo_sm_reserve", 99),
+                     ("collective_timeout_ms", 0), ("no_such_option", 1)]:
+        with pytest.raises(ConfigError):
+            engine.set_option(key, bad)
+
+
 @pytest.mark.parametrize("H,k", [(32, 5), (64, 5), (64, 0), (32, 2)])
 def test_tensor_core_forward_matches_simt_and_oracle(engine, H, k):
     """tcgen05 3xTF32 MLP forward vs the SIMT fp32 kernels vs the fp64 oracle."""
