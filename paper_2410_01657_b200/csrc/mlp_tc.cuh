@@ -404,8 +404,15 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_base_slot;
 
-  if (warp < 8) ptx::regs_inc<224>();
-  else ptx::regs_dec<56>();
+#ifndef HGNN_FWD_EPI_REGS
+#define HGNN_FWD_EPI_REGS 224
+#endif
+  // the CTA's pool is fixed at launch (384 threads x 168): what the control
+  // warpgroup releases is all the epilogue can take
+  constexpr int EPI_REGS = HGNN_FWD_EPI_REGS, CTL_REGS = (384 * 168 - 256 * EPI_REGS) / 128 / 8 * 8;
+  static_assert(256 * EPI_REGS + 128 * CTL_REGS <= 384 * 168 && CTL_REGS >= 24, "setmaxnreg exceeds the CTA pool");
+  if (warp < 8) ptx::regs_inc<EPI_REGS>();
+  else ptx::regs_dec<CTL_REGS>();
 
   if (warp < 8) {
     // ------------------------------------------------------------ epilogue
