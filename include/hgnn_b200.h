@@ -233,8 +233,6 @@ int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double
  * "encoder_impl":      1 = (default, H = 64 with both MLP impls 1) node / edge
  *                      encoders on the tcgen05 MLP kernels (zero-padded F-feature
  *                      input, skip + output LayerNorm in the epilogue); 0 = SIMT.
- * "mlp_backward_split": 1 = 16-warp split-row backward epilogue (measured slower,
- *                      default 0).
  * "memory_lean":       -1 = (default) auto, 0 = standard plan, 1 = lean plan.
  * "collective_check", "collective_timeout_ms": debug collective-sequence guard. 
  * "halo_overlap":      1 = (default; R > 1, exchange mode set, tcgen05 path) forward:

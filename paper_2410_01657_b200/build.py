@@ -32,7 +32,7 @@ CXXFLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-Xcompiler
 
 SOURCES = ["engine.cu", "model.cu", "host_graph.cpp", "host_params.cpp"]
 DEBUG_SOURCES = ["selftest.cu"]
-HEADERS = ["common.hpp", "engine_ctx.hpp", "local_group.hpp", "mlp_generic.cuh", "model_kernels.cuh", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "mlp_tc_bwd_cs.cuh", "tc_ptx.cuh", "edge_fact.cuh", "encoder_tc.cuh"]
+HEADERS = ["common.hpp", "engine_ctx.hpp", "local_group.hpp", "mlp_generic.cuh", "model_kernels.cuh", "graph_kernels.cuh", "mlp_simt.cuh", "mlp_tc.cuh", "mlp_tc_bwd.cuh", "tc_ptx.cuh", "edge_fact.cuh", "encoder_tc.cuh"]
 
 
 def _newer(src: list[Path], out: Path) -> bool:

@@ -26,7 +26,6 @@
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
 #include "mlp_tc_bwd.cuh"
-#include "mlp_tc_bwd_cs.cuh"
 
 using namespace hgnn_b200;
 using namespace hgnn_b200::engine;
@@ -771,14 +770,6 @@ int launch_tc_backward(hgnn_ctx* c, int mode, int64_t m, const TcBwdArgs& in) {
     auto k32 = edge ? mlp_tc_backward_kernel<kEdgeInput, false, 32> : mlp_tc_backward_kernel<kNodeInput, false, 32>;
     CUDA_OK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCfg::SMEM));
     k32<<<grid, TcBwdCfg::THREADS, TcBwdCfg::SMEM, c->stream>>>(args);
-    check_launch(c);
-    return grid;
-  }
-  if (c->bwd_split && !prof) {  // split-row epilogue (mlp_tc_bwd_cs.cuh)
-    auto ks = mode == kEdgeFact ? mlp_tc_backward_cs_kernel<kEdgeFact>
-                                : (edge ? mlp_tc_backward_cs_kernel<kEdgeInput> : mlp_tc_backward_cs_kernel<kNodeInput>);
-    CUDA_OK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcBwdCsCfg::SMEM));
-    ks<<<grid, TcBwdCsCfg::THREADS, TcBwdCsCfg::SMEM, c->stream>>>(args);
     check_launch(c);
     return grid;
   }
@@ -1726,9 +1717,6 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value < -1 || value > 1) fail(HGNN_ERR_CONFIG, "memory_lean: -1 (auto), 0 or 1");
       c->lean_opt = (int)value;
       for (auto& v : c->plan_key) v = -1;  // re-plan at the next call
-    } else if (k == "mlp_backward_split") {
-      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "mlp_backward_split: 0 or 1");
-      c->bwd_split = (int)value;
     } else if (k == "collective_check") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "collective_check: 0 or 1");
       c->coll_check = (int)value;

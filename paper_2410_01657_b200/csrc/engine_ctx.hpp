@@ -118,7 +118,6 @@ struct hgnn_ctx {
   hgnn_b200::DevBuf<double> grads;
   int fwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H in {32, 64})
   int bwd_impl = 1;                     // 0 = SIMT, 1 = tcgen05 (H = 64)
-  int bwd_split = 0;                    // option "mlp_backward_split": 16-warp split-row epilogue (measured slower, off)
   hgnn_b200::DevBuf<float> bchunks;                // backward chunk sequence per MLP
   std::vector<int64_t> bchunk_off;
   hgnn_b200::DevBuf<float> tc_scratch;

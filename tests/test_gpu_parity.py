@@ -176,7 +176,7 @@ def test_option_values_are_validated(engine):
     (the engine's state is unchanged)."""
     from paper_2410_01657_b200 import ConfigError
     for key, bad in [("edge_factorized", 2), ("memory_lean", 3), ("encoder_impl", -1), ("tma_gather", 5),
-                     ("mlp_backward_split", 2), ("mlp_backward_impl", 7), ("halo_sm_reserve", 99),
+                     ("mlp_backward_split", 0), ("mlp_backward_impl", 7), ("halo_sm_reserve", 99),
                      ("collective_timeout_ms", 0), ("no_such_option", 1)]:
         with pytest.raises(ConfigError):
             engine.set_option(key, bad)
