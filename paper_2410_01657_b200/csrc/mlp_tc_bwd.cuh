@@ -91,6 +91,9 @@ constexpr bool kDwN128 = HGNN_DW_N128;
 #ifndef HGNN_PK_TMEM
 #define HGNN_PK_TMEM 0
 #endif
+#ifndef HGNN_LNB_KEEP_T
+#define HGNN_LNB_KEEP_T 0  // 1: the LayerNorm-adjoint's second pass reads t_l from registers, not L1 (A/B knob)
+#endif
 #ifndef HGNN_BWD_PREFETCH
 #define HGNN_BWD_PREFETCH 0  // 1: input-segment gathers one step ahead (behind the MMA / dX wait): measured neutral at C3 (edge 67.4 ms, node 9.85 vs 9.5 ms)
 #endif
@@ -704,12 +707,17 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
           }
           } else {
           float p1[8], p2[8];
+          float tk[HGNN_LNB_KEEP_T ? 64 : 1];  // HGNN_LNB_KEEP_T: t_l kept in registers for pass 2
 #pragma unroll
           for (int i = 0; i < 8; ++i) p1[i] = p2[i] = 0.f;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
             const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+            if (HGNN_LNB_KEEP_T) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) tk[(4 * q + u) % (HGNN_LNB_KEEP_T ? 64 : 1)] = tv[u];
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int jx = 4 * q + u;
@@ -729,7 +737,11 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
               (((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]))) * (1.0f / HL);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float4 t4 = (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
+            const float4 t4 = HGNN_LNB_KEEP_T ? make_float4(tk[(4 * q) % (HGNN_LNB_KEEP_T ? 64 : 1)],
+                                                            tk[(4 * q + 1) % (HGNN_LNB_KEEP_T ? 64 : 1)],
+                                                            tk[(4 * q + 2) % (HGNN_LNB_KEEP_T ? 64 : 1)],
+                                                            tk[(4 * q + 3) % (HGNN_LNB_KEEP_T ? 64 : 1)])
+                              : (kExp & 2) ? make_float4(0.5f, -0.5f, 0.25f, -0.25f) : ptx::ld_hint(st + q * 128, keep);
             if (4 * q >= HL) {  // zero padding
               dh[4 * q] = dh[4 * q + 1] = dh[4 * q + 2] = dh[4 * q + 3] = 0.f;
               continue;
