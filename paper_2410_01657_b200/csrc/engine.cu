@@ -1405,6 +1405,8 @@ int hgnn_graph_upload(hgnn_ctx* c, const hgnn_graph_desc* g) {
       const bool empty_recv = c->h_recv_off[(size_t)n + 1] == c->h_recv_off[(size_t)n];
       const int64_t base = empty_recv ? nl : g->recv_rows[c->h_recv_off[(size_t)n]];
       c->h_recv_base[(size_t)n] = base;
+      if (!empty_recv && (base < nl || base + (c->h_recv_off[(size_t)n + 1] - c->h_recv_off[(size_t)n]) > rows))
+        fail(HGNN_ERR_INTEGRITY, "recv rows must be halo rows [num_local, rows)");
       for (int32_t t = c->h_recv_off[(size_t)n]; t < c->h_recv_off[(size_t)n + 1]; ++t)
         if (g->recv_rows[t] != base + (t - c->h_recv_off[(size_t)n]))
           fail(HGNN_ERR_INTEGRITY, "recv rows of a neighbour must be one consecutive block (graph.cpp:184-201)");
