@@ -227,6 +227,8 @@ int hgnn_train_step(hgnn_ctx* ctx, double lr, double beta1, double beta2, double
  *                     0 = SIMT fp32 kernels.
  * "mlp_backward_impl": 1 = tcgen05 tensor-core MLP backward (default, H in {32, 64};
  *                      H = 32 runs zero-padded on the 64-wide kernel), 0 = SIMT fp32.
+ * "adjoint_presum":    1 = the factorised path's node-level input adjoint reads segment
+ *                      sums precomputed by a separate kernel; 0 = (default) in-kernel.
  * "tma_gather":        1 = the fused edge forward's input rows gathered by TMA
  *                      tile::gather4 into SMEM (H = 64); 0 = (default, measured
  *                      faster) per-thread 256-bit row loads into registers.

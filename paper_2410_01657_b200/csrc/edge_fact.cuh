@@ -98,12 +98,14 @@ constexpr size_t edge_proj_smem() { return (size_t)(H * 2 * H + H * (kFactRows +
 // per-block partials part[block][k * 2H + j] (fixed ownership, nodes in
 // order): reduced in block order by grad_reduce_add_kernel after a reorder
 // into W0's row layout (k x H blocks).
-template <int H>
+// PRE_S: the segment sums come precomputed (seg_sum_kernel, rows x 2H in
+// `pre_s`) and are read as coalesced rows instead of gathered here.
+template <int H, bool PRE_S = false>
 __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
     const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ dx_node,
     const float* __restrict__ w0, const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
     const int32_t* __restrict__ twin, int64_t rows, int64_t n_local, float* __restrict__ dx,
-    float* __restrict__ part) {
+    float* __restrict__ part, const float* __restrict__ pre_s = nullptr) {
   static_assert(H == 64, "the factorised edge path is built for H = 64");
   constexpr int NS = 2 * H;  // S width
   constexpr int WK = 4;      // dW: thread owns 4 k-rows x 8 j-columns (16 x 16 thread grid)
@@ -124,6 +126,14 @@ __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
     for (int b = 0; b < WJ; ++b) accw[a][b] = 0.f;
   for (int64_t base = (int64_t)blockIdx.x * kFactRows; base < rows; base += (int64_t)gridDim.x * kFactRows) {
     __syncthreads();
+    if (PRE_S) {
+      for (int t = threadIdx.x; t < kFactRows * NS / 4; t += blockDim.x) {
+        const int r = t / (NS / 4), c4 = t % (NS / 4);
+        const int64_t i = base + r;
+        *reinterpret_cast<float4*>(sr + r * NS + 4 * c4) =
+            i < rows ? __ldg(reinterpret_cast<const float4*>(pre_s + i * NS) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else
     // segment sums, item (r, c4): lanes 0-15 of a warp read the twin row
     // (S_src), lanes 16-31 the slot row (S_dst): 256-byte coalesced pieces.
     // A thread owns column piece c4 of rows r0, r0 + 8, ..., r0 + 56 and walks
@@ -230,6 +240,37 @@ __global__ void __launch_bounds__(kFactThreads) edge_input_adjoint_kernel(
       ps[(j < H ? 0 : H * H) + k * H + (j % H)] = accw[a][b];
     }
 }
+// S = [S_src | S_dst] for every row, one thread per (row, 16-byte piece):
+// the same sums in the same slot order as the in-kernel gather (bitwise), at
+// full occupancy (the adjoint kernel's own gather runs at 2 blocks per SM).
+template <int H>
+__global__ void seg_sum_kernel(const float* __restrict__ dy, const int32_t* __restrict__ beg,
+                               const int32_t* __restrict__ end, const int32_t* __restrict__ twin, int64_t rows,
+                               float* __restrict__ S) {
+  constexpr int Q = 2 * H / 4;  // 16-byte pieces per S row
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= rows * Q) return;
+  const int64_t i = tid / Q;
+  const int c4 = (int)(tid % Q);
+  const bool src_half = c4 < H / 4;
+  const int cc = src_half ? c4 : c4 - H / 4;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int32_t p1 = __ldg(end + i);
+  for (int32_t p = __ldg(beg + i); p < p1; p += 4) {  // 4 slots in flight; +0 padding is bitwise neutral
+    int64_t e[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      e[u] = p + u < p1 ? (src_half ? (int64_t)__ldg(twin + p + u) : (int64_t)(p + u)) : (int64_t)-1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 v =
+          e[u] >= 0 ? __ldg(reinterpret_cast<const float4*>(dy + e[u] * H) + cc) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s = make_float4(s.x + v.x, s.y + v.y, s.z + v.z, s.w + v.w);
+    }
+  }
+  reinterpret_cast<float4*>(S + i * 2 * H)[c4] = s;
+}
+
 template <int H>
 constexpr size_t edge_input_adjoint_smem() {
   return (size_t)(2 * H * H + kFactRows * 2 * H + kFactRows * H) * 4;

@@ -1103,10 +1103,23 @@ void layer_backward(hgnn_ctx* c, int64_t m) {
     Timed t(c, HGNN_K_DX);
     const float* w0 = layer_params(c, m, true).p;
     constexpr size_t smem = edge_input_adjoint_smem<64>();
-    CUDA_OK(cudaFuncSetAttribute(edge_input_adjoint_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    edge_input_adjoint_kernel<64><<<c->fact_blocks, kFactThreads, smem, c->stream>>>(
-        c->dsrc.p, x, dxn, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
+    if (c->adj_presum) {  // segment sums at full occupancy into the (now dead) node projection of layer m
+      float* S = proj_buf(c, m);
+      seg_sum_kernel<64><<<blocks_for(c->rows * 2 * H / 4), kEwThreads, 0, c->stream>>>(
+          c->dsrc.p, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, S);
+      check_launch(c);
+      if (c->lean) std::fill(c->ps_ready.begin(), c->ps_ready.end(), 0);
+      else c->ps_ready[(size_t)m] = 0;  // a repeated backward recomputes P_m
+      CUDA_OK(cudaFuncSetAttribute(edge_input_adjoint_kernel<64, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      edge_input_adjoint_kernel<64, true><<<c->fact_blocks, kFactThreads, smem, c->stream>>>(
+          c->dsrc.p, x, dxn, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p, S);
+    } else {
+      CUDA_OK(cudaFuncSetAttribute(edge_input_adjoint_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      edge_input_adjoint_kernel<64><<<c->fact_blocks, kFactThreads, smem, c->stream>>>(
+          c->dsrc.p, x, dxn, w0, c->seg_beg.p, c->seg_end.p, c->twin.p, c->rows, c->nl, c->dx.p, c->fact_part.p);
+    }
     check_launch(c);
     const int64_t nw = 2 * H * H;  // W0 rows 0 .. 2H-1 (x_src, x_dst blocks) of the edge MLP
     grad_reduce_add_kernel<<<blocks_for(nw), kEwThreads, 0, c->stream>>>(c->fact_part.p, c->fact_blocks, nw,
@@ -1726,6 +1739,9 @@ int hgnn_set_option(hgnn_ctx* c, const char* key, int64_t value) {
       if (value <= 0) fail(HGNN_ERR_CONFIG, "collective_timeout_ms must be positive");
       c->coll_timeout_ms = value;
       if (c->group) c->group->timeout_ms = value;
+    } else if (k == "adjoint_presum") {
+      if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "adjoint_presum: 0 or 1");
+      c->adj_presum = (int)value;
     } else if (k == "tma_gather") {
       if (value != 0 && value != 1) fail(HGNN_ERR_CONFIG, "tma_gather: 0 (per-thread row loads) or 1 (TMA gather4)");
       c->tma_gather = (int)value;

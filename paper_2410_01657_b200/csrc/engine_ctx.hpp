@@ -128,6 +128,7 @@ struct hgnn_ctx {
   // the fused edge kernel ([0, n_tiles_bnd) cover the boundary slots), rows
   // with an empty segment (zeroed aggregate), node projections per layer
   int edge_fact = 1;              // option "edge_factorized" (default on: measured faster at C3)
+  int adj_presum = 0;             // option "adjoint_presum": node-level adjoint with precomputed segment sums (measured slower, off)
   int tma_gather = 0;             // option "tma_gather": fused edge forward input rows by TMA tile::gather4 (H = 64; measured slower, off)
   bool fact_ok = false;           // every receiver segment fits one 128-slot tile
   hgnn_b200::DevBuf<int32_t> tiles, rows_empty;

@@ -176,7 +176,7 @@ def test_option_values_are_validated(engine):
     (the engine's state is unchanged)."""
     from paper_2410_01657_b200 import ConfigError
     for key, bad in [("edge_factorized", 2), ("memory_lean", 3), ("encoder_impl", -1), ("tma_gather", 5),
-                     ("mlp_backward_split", 0), ("mlp_backward_impl", 7), ("halo_sm_reserve", 99),
+                     ("mlp_backward_split", 0), ("adjoint_presum", 2), ("mlp_backward_impl", 7), ("halo_sm_reserve", 99),
                      ("collective_timeout_ms", 0), ("no_such_option", 1)]:
         with pytest.raises(ConfigError):
             engine.set_option(key, bad)
@@ -325,3 +325,32 @@ def test_tma_gathered_forward_is_bitwise_equal(engine, E, p, M, k, fact):
         assert np.asarray(u).tobytes() == np.asarray(v).tobytes()
     ref = O.oracle_mp_run([g], H, M, k, "na2a", mp, [x0], [e0], [dx], [de])
     assert rel(res[1][0], ref["x_out"][0][M - 1]) < FWD_TOL
+
+
+def test_presummed_node_adjoint_is_bitwise_equal(engine):
+    """Node-level input adjoint of the factorised path with the segment sums
+    precomputed at full occupancy (adjoint_presum 1) against the in-kernel
+    gather (0, default): same sums in the same slot order, bitwise equal
+    adjoints and gradients; a repeated backward recomputes the node projection
+    whose buffer held the sums."""
+    H, M, k = 64, 2, 3
+    cfg = GnnConfig("ps", H, M, k, mode="na2a")
+    g = build_rank_graph(4, 3, 1, 0, "verify")
+    mp = mp_params(cfg, init_params(cfg, 51))
+    x0, e0, dx, de = random_inputs(g, H, 29)
+    res = {}
+    for ps in (1, 0):
+        engine.upload_graph(g)
+        engine.configure(cfg)
+        engine.upload_params(mp)
+        engine.set_option("edge_factorized", 1)
+        engine.set_option("adjoint_presum", ps)
+        engine.nmp_forward(x0, e0)
+        res[ps] = tuple(engine.nmp_backward(dx, de))
+        if ps:
+            again = tuple(engine.nmp_backward(dx, de))
+            for u, v in zip(res[ps], again):
+                assert u.tobytes() == v.tobytes()
+    engine.set_option("adjoint_presum", 0)
+    for u, v in zip(res[1], res[0]):
+        assert u.tobytes() == v.tobytes()
