@@ -91,6 +91,9 @@ constexpr bool kDwN128 = HGNN_DW_N128;
 #ifndef HGNN_PK_TMEM
 #define HGNN_PK_TMEM 0
 #endif
+#ifndef HGNN_SCRATCH_KEEP
+#define HGNN_SCRATCH_KEEP 1  // recompute scratch stored evict_last (C3: step 336 -> 332.5 ms; round 1 measured it neutral)
+#endif
 #ifndef HGNN_LNB_KEEP_T
 #define HGNN_LNB_KEEP_T 0  // 1: the LayerNorm-adjoint's second pass reads t_l from registers, not L1 (A/B knob)
 #endif
@@ -605,8 +608,11 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
         const float inv_std = (kExp & 8) ? 1.0f : ln0_pad<HL>(u);
         float4* st = scr + (int64_t)(l - 1) * 16 * 128 + trow;
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          st[q * 128] = make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+        for (int q = 0; q < 16; ++q) {
+          const float4 tq = make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+          if (HGNN_SCRATCH_KEEP) ptx::st_hint(st + q * 128, tq, keep);  // A/B knob: evict_last scratch lines
+          else st[q * 128] = tq;
+        }
         scr_inv[(l - 1) * 128 + trow] = inv_std;
         add_elu<H>(h, u);
       }
