@@ -210,8 +210,11 @@ __device__ __forceinline__ void tc_signal(uint64_t* bar) {
 #define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py); bits 32: input gathers dropped, 64: no e' stores, 128: no reducer work
 #endif
 
+// pol != 0: L2 cache-hint policy of the row loads (the backward keeps rows it
+// gathers twice, evict_last, and streams the second read, evict_first)
 template <int H, int MODE>
-__device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool valid, int c, float (&v)[H]) {
+__device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool valid, int c, float (&v)[H],
+                                          uint64_t pol = 0) {
   if (HGNN_EXP & 32) valid = false;
   if (MODE == kEncoder) {  // in_dim (<= 8) features, zero-padded to H
 #pragma unroll
@@ -239,8 +242,13 @@ __device__ __forceinline__ void tc_gather(const TcFwdArgs& a, int64_t row, bool 
 #define HGNN_LDG256 1
 #endif
     if (HGNN_LDG256) {
+      if (pol) {
 #pragma unroll
-      for (int j = 0; j < H / 8; ++j) ptx::ldg256(seg + 8 * j, v + 8 * j);
+        for (int j = 0; j < H / 8; ++j) ptx::ldg256_hint(seg + 8 * j, v + 8 * j, pol);
+      } else {
+#pragma unroll
+        for (int j = 0; j < H / 8; ++j) ptx::ldg256(seg + 8 * j, v + 8 * j);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < H / 4; ++j) {

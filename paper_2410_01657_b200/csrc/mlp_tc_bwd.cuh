@@ -91,6 +91,9 @@ constexpr bool kDwN128 = HGNN_DW_N128;
 #ifndef HGNN_PK_TMEM
 #define HGNN_PK_TMEM 0
 #endif
+#ifndef HGNN_GATHER_HINT
+#define HGNN_GATHER_HINT 1  // edge modes: recompute gathers evict_last, the dW0 re-gathers evict_first (C3 edge bwd 53.2 -> 52.35 ms)
+#endif
 #ifndef HGNN_SCRATCH_KEEP
 #define HGNN_SCRATCH_KEEP 1  // recompute scratch stored evict_last (C3: step 336 -> 332.5 ms; round 1 measured it neutral)
 #endif
@@ -157,7 +160,8 @@ __device__ __forceinline__ void bwd_row(const float* p, float (&v)[64]) {
 }
 
 template <int MODE, int HL = 64>
-__device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64]) {
+__device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool valid, int c, float (&v)[64],
+                                           uint64_t pol = 0) {
   if (HGNN_EXP & 16) valid = false;
   if (HL != 64) {  // kEdgeInput / kNodeInput rows of width HL, zero-padded
     if (!valid) {
@@ -182,7 +186,9 @@ __device__ __forceinline__ void bwd_gather(const TcBwdArgs& a, int64_t row, bool
   f.a = a.a;
   f.in_dim = a.in_dim;
   f.out_dim = a.out_dim;
-  tc_gather<64, MODE>(f, row, valid, c, v);
+  // edge modes: the rows are gathered twice (recompute, dW0 operand); node rows are contiguous streams
+  constexpr bool hint = HGNN_GATHER_HINT && (MODE == kEdgeInput || MODE == kEdgeFact);
+  tc_gather<64, MODE>(f, row, valid, c, v, hint ? pol : 0);
 }
 __device__ __forceinline__ void bwd_gather_proj(const TcBwdArgs& a, int64_t row, bool valid, float (&v)[64]) {
   TcFwdArgs f{};
@@ -572,14 +578,14 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
       const long long tr0 = PROF ? clock64() : 0;
       // ---------------------------------------------- forward recompute
       // (segment c + 1 is gathered while the MMA of segment c runs)
-      if (!HGNN_BWD_PREFETCH || !h_ready) bwd_gather<MODE, HL>(a, row, valid, 0, h);
+      if (!HGNN_BWD_PREFETCH || !h_ready) bwd_gather<MODE, HL>(a, row, valid, 0, h, keep);
 #pragma unroll 1
       for (int c = 0; c < nseg; ++c) {
         if (c > 0) {
           ptx::mbar_wait(&a_empty[g], pe);
           pe ^= 1;
           ptx::tc_fence_after();
-          if (!HGNN_BWD_PREFETCH) bwd_gather<MODE, HL>(a, row, valid, c, h);
+          if (!HGNN_BWD_PREFETCH) bwd_gather<MODE, HL>(a, row, valid, c, h, keep);
         }
         bwd_store_a(t_ahi, t_alo, h);
         tc_signal(&a_full[g]);
@@ -780,7 +786,7 @@ __global__ void __launch_bounds__(TcBwdCfg::THREADS, 1) mlp_tc_backward_kernel(T
 #pragma unroll
           for (int q = 0; q < 8; ++q) ptx::stg256_hint(a.dy_out + row * H + 8 * q, dh + 8 * q, once);
         }
-        if (c >= 0 && !HGNN_BWD_PREFETCH) bwd_gather<MODE, HL>(a, row, valid, c, h);  // dW0 segment operand
+        if (c >= 0 && !HGNN_BWD_PREFETCH) bwd_gather<MODE, HL>(a, row, valid, c, h, once);  // dW0 segment operand
         stage_chunk(h, dh);
         if (HGNN_BWD_PREFETCH && jb >= K) {  // h is dead: fetch the next dW0 segment operand, or the next
           if (c + 1 < nseg) {                // tile's first input segment, behind the dX wait
