@@ -206,6 +206,9 @@ __device__ __forceinline__ void tc_signal(uint64_t* bar) {
   if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar);
 }
 
+#ifndef HGNN_FWD_STREAM_HINT
+#define HGNN_FWD_STREAM_HINT 0
+#endif
 #ifndef HGNN_EXP
 #define HGNN_EXP 0  // timing experiments only (scripts/build_exp.py); bits 32: input gathers dropped, 64: no e' stores, 128: no reducer work
 #endif
@@ -419,6 +422,13 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
   // warpgroup releases is all the epilogue can take
   constexpr int EPI_REGS = HGNN_FWD_EPI_REGS, CTL_REGS = (384 * 168 - 256 * EPI_REGS) / 128 / 8 * 8;
   static_assert(256 * EPI_REGS + 128 * CTL_REGS <= 384 * 168 && CTL_REGS >= 24, "setmaxnreg exceeds the CTA pool");
+  // HGNN_FWD_STREAM_HINT: the slots' own e rows (read once) and e' (read by the
+  // next layer only) go through L2 evict_first, keeping it for the reused
+  // node rows / projections
+  const uint64_t stream_pol = HGNN_FWD_STREAM_HINT ? ptx::policy_evict_first() : 0;
+  auto fwd_e_pol = [&](int c) -> uint64_t {
+    return (HGNN_FWD_STREAM_HINT && (FACT || (MODE == kEdgeFused && c == 2))) ? stream_pol : 0;
+  };
   if (warp < 8) ptx::regs_inc<EPI_REGS>();
   else ptx::regs_dec<CTL_REGS>();
 
@@ -472,7 +482,7 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
     if (!TMAG && pair < n_pairs) {
       int64_t b0, e0;
       tile_rows(2 * pair + g, b0, e0);
-      tc_gather<H, MODE>(a, b0 + trow, b0 + trow < e0, 0, v);
+      tc_gather<H, MODE>(a, b0 + trow, b0 + trow < e0, 0, v, fwd_e_pol(0));
     }
     for (; pair < n_pairs; pair += gridDim.x) {
       int64_t tb, te;
@@ -494,7 +504,7 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
         if (TMAG) read_seg(valid);
         tc_store_a<H>(t_ahi, t_alo, v);
         signal_a();
-        if (!TMAG && c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v);
+        if (!TMAG && c + 1 < nseg) tc_gather<H, MODE>(a, row, valid, c + 1, v, fwd_e_pol(c + 1));
       }
       if (FACT) tc_gather_proj<H>(a, row, valid, v);  // node-end projections, during the e W0_e MMA
       wait_d();
@@ -536,7 +546,7 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
       if (!TMAG && next < n_pairs) {
         int64_t nb, ne_;
         tile_rows(2 * next + g, nb, ne_);
-        tc_gather<H, MODE>(a, nb + trow, nb + trow < ne_, 0, v);
+        tc_gather<H, MODE>(a, nb + trow, nb + trow < ne_, 0, v, fwd_e_pol(0));
       }
       wait_d();
       const long long t_out0 = PROF ? clock64() : 0;
@@ -718,7 +728,14 @@ __device__ __forceinline__ void mlp_tc_forward_body(const TcFwdArgs& a, const CU
           float* eo = (a.out && !(HGNN_EXP & 64)) ? a.out + (tb + r) * H + CPL * lane : nullptr;  // nullptr: e' not stored (dead)
           if (CPL == 2) {
             const float2 y = *reinterpret_cast<const float2*>(yt + ytile_off<H>(r, lane / 2) + 8 * (lane & 1));
-            if (eo) *reinterpret_cast<float2*>(eo) = y;
+            if (eo) {
+              if (HGNN_FWD_STREAM_HINT)
+                asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(eo), "f"(y.x), "f"(y.y),
+                             "l"(stream_pol)
+                             : "memory");
+              else
+                *reinterpret_cast<float2*>(eo) = y;
+            }
             acc[0] = fmaf(w, y.x, acc[0]);
             acc[CPL - 1] = fmaf(w, y.y, acc[CPL - 1]);
           } else {
